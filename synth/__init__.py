@@ -1,0 +1,207 @@
+"""Seeded synthetic inputs for the TAPER hot path.
+
+This module is shared by the tests, bench.py and smoke(); it serves both the
+oracle and the CUDA path and therefore holds NONE of the method's arithmetic:
+no latency model, no budget, no admission, no attention.  It only draws batch
+states (lengths, fanouts, slack), paged KV layouts and bf16 tensors from seeded
+generators, following the recipe in DESIGN.md "Input recipe" (which restates
+SURVEY.md Sec. 8(d)):
+
+* Qwen3-32B attention shape: 64 Q heads, 8 KV heads, head_dim 128
+  (App. D "Model"); page size 64; HND page pool
+  [num_pages, h_kv, page, 128] bf16.
+* Fanout pmf matched to Table 4 (P10..P90 = 2,3,4,5,7).
+* Serial requests: one ready slot with branch-local length 0 (the whole
+  context is the "shared" segment).  Parallel requests: n_r ready branches
+  sharing the request's prefix P (+) H, each with its own local tokens.
+* Slack: the most urgent request gets exactly ``slack_min_ms``; the others
+  ``slack_min_ms + U[0, slack_spread_ms]``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+Q_HEADS = 64
+KV_HEADS = 8
+HEAD_DIM = 128
+GROUP = Q_HEADS // KV_HEADS
+PAGE = 64
+N_LAYERS = 64
+
+# Table 4 matched pmf; SURVEY.md Sec. 8(d).
+FANOUT_PMF = {2: .20, 3: .25, 4: .25, 5: .15, 6: .04, 7: .04, 8: .03, 9: .02, 10: .02}
+
+
+@dataclass
+class Batch:
+    """Batch state in the C-ABI's SoA form (all host numpy arrays)."""
+    req_shared_len: np.ndarray   # int32 [R]   Lsh_r
+    req_slot_off: np.ndarray     # int32 [R+1] CSR of ready slots
+    req_slack_ms: np.ndarray     # float64 [R] d_r(t) - t
+    slot_local_len: np.ndarray   # int32 [S]   Lloc_s
+    req_serial: np.ndarray = field(default=None)  # bool [R] (info only)
+
+    @property
+    def n_req(self) -> int:
+        return int(self.req_shared_len.shape[0])
+
+    @property
+    def n_slot(self) -> int:
+        return int(self.slot_local_len.shape[0])
+
+
+@dataclass
+class Layout:
+    """Paged KV layout: page lists of every shared and local segment."""
+    page_size: int
+    num_pages: int
+    req_page_off: np.ndarray   # int32 [R+1]
+    req_pages: np.ndarray      # int32
+    slot_page_off: np.ndarray  # int32 [S+1]
+    slot_pages: np.ndarray     # int32
+
+
+def _csr(counts) -> np.ndarray:
+    off = np.zeros(len(counts) + 1, np.int64)
+    off[1:] = np.cumsum(counts)
+    return off.astype(np.int32)
+
+
+def make_batch(shared_lens, fanouts, local_lens, slack_min_ms=30.0, slack_spread_ms=20.0,
+               serial=None, rng=None) -> Batch:
+    """Assemble a Batch.  ``fanouts[r]`` ready slots for request r; ``local_lens`` is the
+    flat list of Lloc over all slots.  The slack of a random request is exactly
+    ``slack_min_ms``; the others get ``+ U[0, slack_spread_ms]``."""
+    rng = rng or np.random.default_rng(0)
+    R = len(shared_lens)
+    slack = slack_min_ms + rng.uniform(0.0, slack_spread_ms, size=R)
+    if R:
+        slack[rng.integers(R)] = slack_min_ms
+    return Batch(np.asarray(shared_lens, np.int32), _csr(fanouts), slack.astype(np.float64),
+                 np.asarray(local_lens, np.int32),
+                 np.asarray(serial if serial is not None else [f == 1 for f in fanouts], bool))
+
+
+def sample_fanout(rng, n) -> np.ndarray:
+    ks = np.array(list(FANOUT_PMF.keys()))
+    ps = np.array(list(FANOUT_PMF.values()))
+    return rng.choice(ks, size=n, p=ps / ps.sum())
+
+
+def config_batch(name: str, seed: int = 0, slack_min_ms: float = 1e3,
+                 slack_spread_ms: float = 20.0) -> Batch:
+    """The BASELINE.json configs as batch states.
+
+    c1: tiny -- r0 serial (Lsh 512), r1 parallel with 4 branches of Lloc 32.
+    c2: 64 requests, 32 serial + 32 parallel (n_r ~ U{2..8}), Lsh 4096, Lloc ~ U{1..256}.
+    c3: 32 requests, 16 serial + 16 parallel (n_r ~ U{8..16}), Lsh ~ U[16384, 32768],
+        Lloc ~ U{1..512}.
+    c5: 256 requests, 128 serial + 128 parallel (Table-4 fanout pmf),
+        Lsh log-uniform [1024, 32768], Lloc ~ U{1..256}.
+    Serial/parallel requests are interleaved in a seeded random order.
+    """
+    rng = np.random.default_rng(seed)
+    if name == "c1":
+        return make_batch([512, 512], [1, 4], [0, 32, 32, 32, 32], slack_min_ms,
+                          slack_spread_ms, rng=rng)
+    if name == "c2":
+        n_ser, n_par = 32, 32
+        lsh = lambda n: np.full(n, 4096)
+        fan = lambda n: rng.integers(2, 9, size=n)
+        lloc_hi = 256
+    elif name == "c3":
+        n_ser, n_par = 16, 16
+        lsh = lambda n: rng.integers(16384, 32769, size=n)
+        fan = lambda n: rng.integers(8, 17, size=n)
+        lloc_hi = 512
+    elif name == "c5":
+        n_ser, n_par = 128, 128
+        lsh = lambda n: np.exp(rng.uniform(np.log(1024), np.log(32768), size=n)).astype(np.int64)
+        fan = lambda n: sample_fanout(rng, n)
+        lloc_hi = 256
+    else:
+        raise ValueError(f"unknown config {name!r}")
+    kinds = np.array([True] * n_ser + [False] * n_par)
+    rng.shuffle(kinds)
+    R = len(kinds)
+    shared = lsh(R)
+    fanouts = np.where(kinds, 1, fan(R))
+    local = []
+    for r in range(R):
+        if kinds[r]:
+            local.append(0)
+        else:
+            local.extend(rng.integers(1, lloc_hi + 1, size=int(fanouts[r])).tolist())
+    return make_batch(shared, fanouts, local, slack_min_ms, slack_spread_ms, serial=kinds,
+                      rng=rng)
+
+
+def random_small_batch(rng, max_req=6, max_fanout=5, max_shared=4096, max_local=64,
+                       slack_range=(5.0, 60.0)) -> Batch:
+    """Small random batch for admission fuzzing (ties in Lloc are likely)."""
+    R = int(rng.integers(1, max_req + 1))
+    fanouts = rng.integers(1, max_fanout + 1, size=R)
+    shared = rng.integers(0, max_shared + 1, size=R)
+    local = rng.integers(0, max_local + 1, size=int(fanouts.sum()))
+    b = make_batch(shared, fanouts, local, 0.0, 0.0, rng=rng)
+    b.req_slack_ms = rng.uniform(*slack_range, size=R)
+    return b
+
+
+def make_layout(batch: Batch, page_size: int = PAGE, rng=None, spare_pages: int = 0,
+                local_capacity: int | None = None) -> Layout:
+    """Give every shared segment ceil(Lsh/page) pages and every slot's local segment
+    ceil(max(Lloc, local_capacity)/page) pages, drawn as a random permutation of
+    the pool (so segments are not contiguous)."""
+    rng = rng or np.random.default_rng(1)
+    need_sh = (batch.req_shared_len.astype(np.int64) + page_size - 1) // page_size
+    loc = batch.slot_local_len.astype(np.int64)
+    if local_capacity is not None:
+        loc = np.maximum(loc, local_capacity)
+    need_loc = (loc + page_size - 1) // page_size
+    total = int(need_sh.sum() + need_loc.sum()) + spare_pages
+    perm = rng.permutation(max(total, 1)).astype(np.int32)
+    req_pages = perm[: need_sh.sum()]
+    slot_pages = perm[need_sh.sum(): need_sh.sum() + need_loc.sum()]
+    return Layout(page_size, max(total, 1), _csr(need_sh), np.ascontiguousarray(req_pages),
+                  _csr(need_loc), np.ascontiguousarray(slot_pages))
+
+
+def make_kv(num_pages, h_kv=KV_HEADS, page_size=PAGE, d=HEAD_DIM, seed=0, device="cpu"):
+    """K, V pools [num_pages, h_kv, page, d] bf16 ~ N(0, 1)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    shape = (num_pages, h_kv, page_size, d)
+    k = torch.randn(shape, generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+    v = torch.randn(shape, generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+    return k, v
+
+
+def make_q(n_slot, q_heads=Q_HEADS, d=HEAD_DIM, seed=0, gain=1.0, device="cpu"):
+    """Queries [S, q_heads, d] bf16 ~ N(0, gain^2) ("peaked" variant: gain 4)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed + 7919)
+    q = torch.randn((n_slot, q_heads, d), generator=g, device=device, dtype=torch.float32)
+    return (q * gain).to(torch.bfloat16)
+
+
+def plant_sink(k_pages, q, batch: Batch, layout: Layout, gain: float = 32.0):
+    """"sink" variant: overwrite prefix token 0 of each request and KV head with a key
+    aligned to the mean of that request's queries of the GQA group, so one key
+    dominates the softmax.  In place on CPU tensors."""
+    import torch
+    h_kv = k_pages.shape[1]
+    group = q.shape[1] // h_kv
+    off = batch.req_slot_off
+    for r in range(batch.n_req):
+        if batch.req_shared_len[r] < 1 or off[r + 1] == off[r]:
+            continue
+        page = int(layout.req_pages[layout.req_page_off[r]])
+        for g in range(h_kv):
+            qq = q[off[r]:off[r + 1], g * group:(g + 1) * group].float().reshape(-1, q.shape[2])
+            mean = qq.mean(0)
+            k_pages[page, g, 0] = (gain * mean / mean.norm().clamp_min(1e-6)).to(torch.bfloat16)
