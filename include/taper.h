@@ -1,0 +1,182 @@
+/*
+ * taper.h -- C ABI of the B200-native TAPER hot path (arXiv 2605.06914).
+ *
+ * Two calls follow the paper's problem statement:
+ *   taper_admit            admit(batch state, slack, latency model) -> admitted-branch set
+ *                          Sec. 3.3 "Slack-budgeted admission" and
+ *                          Algorithm 1 "TAPER Per-Step Planner" (L147-181).
+ *   taper_decode_attention decode_attention(admitted set, paged prefix/branch KV, queries)
+ *                          -> per-sequence outputs.  Sec. 3.1 visibility rule (L100-103):
+ *                          a branch token attends to P (+) H (+) h_i (+) y_{i,<t}; the
+ *                          prefix P (+) H is served "from a single set of prefix blocks"
+ *                          (L108).
+ * plus the work-list rebuild used after the admission broadcast on G > 1 GPUs
+ * (taper_build_work) and host helpers.
+ *
+ * Conventions (all calls):
+ *   * Pointers inside the structs are DEVICE pointers unless marked [host].  The caller
+ *     owns every buffer; no call allocates device memory or synchronises the stream.
+ *     Every kernel is enqueued on `stream` (a cudaStream_t passed as void*; NULL = the
+ *     legacy default stream).
+ *   * Return value = host-side validation / launch result (TAPER_OK or a negative
+ *     TAPER_ERR_*).  Data errors that only the device can see are OR-ed into the device
+ *     status word `taper_admission.status` (TAPER_STATUS_* bits); outputs are undefined
+ *     when it is non-zero, and the caller reads it whenever it chooses.
+ *   * Stateless and thread-safe: no globals except a thread-local last-error string.
+ *   * bf16 tensors are passed as void* to raw bf16 storage (no torch or CUDA types here).
+ */
+#ifndef TAPER_H_
+#define TAPER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TAPER_API __attribute__((visibility("default")))
+#else
+#define TAPER_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ----------------------------------------------------------------- return codes */
+#define TAPER_OK 0
+#define TAPER_ERR_ARG (-1)          /* null pointer, negative count, bad struct field     */
+#define TAPER_ERR_RHO (-2)          /* rho outside (0, 1]                 */
+#define TAPER_ERR_NONMONOTONE (-3)  /* b <= 0 or c <= 0 or a < 0 (App. C.1)          */
+#define TAPER_ERR_CAPACITY (-4)     /* R or S > TAPER_MAX_SLOTS, page size unsupported,
+                                       workspace too small                                 */
+#define TAPER_ERR_CUDA (-5)         /* a CUDA launch / driver call failed                 */
+#define TAPER_ERR_UNSUPPORTED (-6)  /* non-linear utility on the device path (round 1)    */
+
+/* ----------------------------------------------------------------- device status bits */
+#define TAPER_STATUS_EMPTY_REQUEST 1   /* a request had no ready slot; it is skipped     */
+#define TAPER_STATUS_BAD_LENGTH 2      /* negative length / CSR offsets not monotone     */
+#define TAPER_STATUS_PRECISION 4       /* c < budget * 2^-46: fp64 may tie candidates of
+                                          different cost, so the sort+scan is no longer
+                                          guaranteed bit-identical to Alg. 1             */
+#define TAPER_STATUS_WORK_OVERFLOW 8   /* attention partials exceed the workspace        */
+
+#define TAPER_MAX_SLOTS 4096   /* capacity of the single-CTA admission kernel (R and S)  */
+#define TAPER_HEAD_DIM 128     /* Qwen3-32B head_dim                     */
+#define TAPER_GQA_GROUP 8      /* 64 Q heads / 8 KV heads (L359)                         */
+#define TAPER_CHUNK_TOKENS 1024 /* shared-prefix split size: a fixed function of the
+                                   prefix length only (schedule invariance, Lemma 1)     */
+
+/* App. C.1 display eq. (L316): T(S) = a + b*n_tokens + c*L_context, in ms. [host]      */
+typedef struct {
+  double a; /* ms, >= 0          */
+  double b; /* ms per sequence, > 0  */
+  double c; /* ms per context token, > 0 */
+} taper_latency_model;
+
+/* Step-width policies: App. D "Baselines" (L393-400) and Alg. 1.                      */
+typedef enum {
+  TAPER_POLICY_OFF = 0,   /* IRP-Off:   w_{r,t} = 1                                   */
+  TAPER_POLICY_CAP = 1,   /* IRP-Ck:    w_{r,t} = min(n_r, cap)                        */
+  TAPER_POLICY_EAGER = 2, /* IRP-Eager: w_{r,t} = n_r                                  */
+  TAPER_POLICY_GREEDY = 3 /* TAPER: Alg. 1 greedy under the slack budget               */
+} taper_policy_kind;
+
+typedef struct {            /* [host] */
+  int32_t kind;             /* taper_policy_kind                                       */
+  int32_t cap;              /* TAPER_POLICY_CAP: k >= 1                                */
+  double rho;               /* slack fraction, (0, 1] (Sec. 3.3; default 0.8 L391) */
+  const double *marginal_utility; /* must be NULL = linear utility u_r(k) = k (L391);
+                                     non-linear curves return TAPER_ERR_UNSUPPORTED    */
+} taper_policy;
+
+/* Batch state, structure-of-arrays (device).  Request r's ready slots are the slot
+ * indices [req_slot_off[r], req_slot_off[r+1]); a serial-stage request has one slot,
+ * a parallel-stage request one slot per exposed-but-incomplete branch (L128).          */
+typedef struct {
+  int32_t n_req;                  /* R  (host value), 0 <= R <= TAPER_MAX_SLOTS       */
+  int32_t n_slot;                 /* S  (host value), 0 <= S <= TAPER_MAX_SLOTS       */
+  const int32_t *req_shared_len;  /* [R]   Lsh_r: tokens of P (+) H (serial: whole ctx) */
+  const int32_t *req_slot_off;    /* [R+1] CSR offsets, req_slot_off[0]=0, [R]=S        */
+  const double *req_slack_ms;     /* [R]   d_r(t) - t in ms (L130)                      */
+  const int32_t *slot_local_len;  /* [S]   Lloc_s: branch-local tokens h_i (+) y_{i,<=t},
+                                     the current token already appended (0 for serial) */
+} taper_batch;
+
+/* Admission outputs (device, caller-allocated).                                         */
+typedef struct {
+  int32_t *req_width;     /* [R] w_{r,t} = 1 + k_r (0 for an empty request)            */
+  uint8_t *slot_admitted; /* [S] 1 iff the slot advances this step                     */
+  int32_t *adm_list;      /* [S] admitted slots in ascending slot index; first n_adm   */
+  int32_t *n_adm;         /* [1]                                                        */
+  double *diag;           /* [5] T0, budget = T0 + rho*B_t, T(S), E = T(S)-T0 (Sec. 2.3
+                             L83-85), min_r slack                                       */
+  int32_t *status;        /* [1] TAPER_STATUS_* bits (0 = OK)                           */
+} taper_admission;
+
+/* One layer's paged KV cache on this rank (device).                                     */
+typedef struct {
+  const void *k_pages;  /* bf16 [num_pages, h_local, page_size, 128], 16-B aligned       */
+  const void *v_pages;  /* bf16 [num_pages, h_local, page_size, 128]                     */
+  int32_t num_pages;
+  int32_t page_size;    /* 16, 32, 64 or 128                                            */
+  int32_t h_local;      /* KV heads held by this rank (8 / G), 1..8                      */
+  const int32_t *req_page_off; /* [R+1] CSR: pages of request r's shared segment        */
+  const int32_t *req_pages;    /* token t of the segment is row t % page_size of page
+                                  req_pages[req_page_off[r] + t / page_size]            */
+  const int32_t *slot_page_off; /* [S+1] CSR: pages of slot s's local segment          */
+  const int32_t *slot_pages;
+} taper_kv;
+
+/* Workspace bytes for a batch of at most n_req requests / n_slot slots on a rank with
+ * h_local KV heads, where max_chunk_slots bounds sum_r w_r * ceil(Lsh_r / 1024) (the
+ * Eager value sum_r n_r * ceil(Lsh_r/1024) is always enough).  [host]                   */
+TAPER_API int taper_workspace_size(int32_t n_req, int32_t n_slot, int32_t h_local,
+                         int64_t max_chunk_slots, size_t *bytes);
+
+/* One admission step (Sec. 3.3 + Alg. 1; fixed policies of App. D), then the attention
+ * work list for this rank (h_local KV heads) is written into `workspace`.
+ * Greedy with linear utility is evaluated as a sort of candidates by (dL, r, slot)
+ * followed by a prefix scan and the budget predicate on T(n0+m, L0+S_m); see DESIGN.md
+ * for why this equals Alg. 1 bit for bit.  fp64, IEEE round-to-nearest, no FMA.
+ * Errors: TAPER_ERR_ARG, _RHO, _NONMONOTONE, _CAPACITY, _UNSUPPORTED, _CUDA.           */
+TAPER_API int taper_admit(const taper_batch *batch, const taper_latency_model *model,
+                const taper_policy *policy, const taper_admission *out, int32_t h_local,
+                void *workspace, size_t workspace_bytes, void *stream);
+
+/* Rebuild adm_list / n_adm / req_width and the work list from slot_admitted alone (used
+ * on every rank after rank 0's slot_admitted is broadcast, so ranks cannot diverge).    */
+TAPER_API int taper_build_work(const taper_batch *batch, const taper_admission *adm, int32_t h_local,
+                     void *workspace, size_t workspace_bytes, void *stream);
+
+/* Cascade decode attention for one layer on this rank.
+ *   q   : bf16 [S, 8*h_local, 128], slot-indexed (RoPE/QK-norm already applied)
+ *   out : bf16 [S, 8*h_local, 128]; written for admitted slots only
+ *   lse : fp32 [S, 8*h_local] natural-log LSE of each row, or NULL
+ *   scale: softmax scale (1/sqrt(128))
+ * Q head j of the rank's local KV head g is q[s, 8*g + j, :] (HF repeat_kv mapping).
+ * The current token's K/V must already be in the cache (local segment, or the shared
+ * segment of a serial request).  Rows of a page past a segment's end must hold finite
+ * values (they are masked from the softmax but pass through the tensor cores).
+ * Errors: TAPER_ERR_ARG, _CAPACITY, _CUDA.                                             */
+TAPER_API int taper_decode_attention(const taper_batch *batch, const taper_admission *adm,
+                           const taper_kv *kv, const void *q, void *out, float *lse,
+                           float scale, void *workspace, size_t workspace_bytes,
+                           void *stream);
+
+/* Profiling hook (bench.py): when `events` is non-NULL, every later
+ * taper_decode_attention call on this thread records events[0] before the shared-prefix
+ * kernel, events[1] between it and the local/merge kernel and events[2] after, on the
+ * call's stream (cudaEvent_t handles passed as void*).  NULL disables.  [host]          */
+TAPER_API int taper_set_profile_events(void *const *events, int n_events);
+
+/* Human-readable text for a TAPER_ERR_* code or TAPER_STATUS_* bit set.  [host]        */
+TAPER_API const char *taper_status_string(int code);
+/* Last error message of this thread (detail of the most recent failing call).  [host]  */
+TAPER_API const char *taper_last_error(void);
+/* Number of kernel launches the most recent taper_admit / taper_decode_attention /
+ * taper_build_work call on this thread enqueued.  [host]                               */
+TAPER_API int taper_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAPER_H_ */

@@ -1,0 +1,446 @@
+// admit.cu -- per-step admission (Sec. 3.3, Algorithm 1) as one CTA on the device.
+//
+// Algorithm 1 widens the protected composition S0 greedily by
+// utility per marginal latency cost and prunes a request once its next branch does not
+// fit the slack budget.  Under the paper's default linear utility (L391) every score is
+// 1 / (EPS + dt) and dt grows with the candidate's added context dL, so the greedy loop
+// commits candidates in ascending (dL, r, slot) order and stops at the first one that
+// does not fit (monotonicity, L120-123).  This kernel therefore evaluates Alg. 1 as
+//     bitonic sort of candidate keys (dL, r, slot)  ->  int64 prefix scan S_m
+//     -> predicate T(n0 + m, L0 + S_m) <= budget  ->  longest feasible prefix,
+// in fp64 with IEEE round-to-nearest and no contraction, which gives the same set and
+// the same T(S) bits as the literal loop.
+// The fixed policies IRP-Off / IRP-Ck / IRP-Eager (App. D) reuse the same
+// canonical order (ascending Lloc, then slot index).  The kernel then emits the
+// attention work list, so the step never round-trips to the host.
+#include "taper_internal.cuh"
+
+namespace taper {
+
+constexpr int kAdmitThreads = 1024;
+constexpr int kPerThread = kMaxSlots / kAdmitThreads;  // 4
+
+struct AdmitParams {
+  int R, S;
+  const int32_t *Lsh, *off, *Lloc;
+  const double *slack;
+  double a, b, c, rho;
+  int kind, cap;
+  int decide;  // 1: admission + work list; 0: work list from slot_admitted only
+  int32_t *req_width;
+  uint8_t *slot_admitted;
+  int32_t *adm_list, *n_adm;
+  double *diag;
+  int32_t *status;
+  int32_t *hdr, *slot_req, *slot_rank, *req_chunk_off, *req_part_off, *req_adm_off,
+      *adm_by_req;
+  int64_t cap_cs;
+  int h_local;
+};
+
+__device__ __forceinline__ double T_eval(double a, double b, double c, long long n,
+                                         long long L) {
+  // App. C.1: T(S) = a + b*n_tokens + c*L_context, each operation rounded separately.
+  return __dadd_rn(__dadd_rn(a, __dmul_rn(b, __ll2double_rn(n))),
+                   __dmul_rn(c, __ll2double_rn(L)));
+}
+
+// Block-wide exclusive scan of 4 consecutive values per thread (4096 elements).
+template <typename T>
+__device__ T block_exscan4(T (&v)[kPerThread], T *warp_buf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T local[kPerThread];
+  T run = 0;
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) { local[k] = run; run += v[k]; }
+  T incl = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) warp_buf[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    T x = warp_buf[lane];
+    T xi = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, xi, d);
+      if (lane >= d) xi += y;
+    }
+    warp_buf[lane] = xi - x;          // exclusive warp offset
+    if (lane == 31) warp_buf[32] = xi;  // total
+  }
+  __syncthreads();
+  T base = warp_buf[warp] + (incl - run);
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) v[k] = base + local[k];
+  T total = warp_buf[32];
+  __syncthreads();
+  return total;
+}
+
+// Ascending bitonic sort of n (power of two, <= 4096) keys in shared memory.
+__device__ void bitonic_sort(unsigned long long *keys, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          unsigned long long x = keys[i], y = keys[ixj];
+          bool up = (i & k) == 0;
+          if ((x > y) == up) { keys[i] = y; keys[ixj] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long x) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+  return x;
+}
+__device__ __forceinline__ double warp_min_d(double x) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) x = fmin(x, __shfl_xor_sync(0xffffffffu, x, d));
+  return x;
+}
+
+__global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) {
+  __shared__ unsigned long long keys[kMaxSlots];
+  __shared__ long long scan_ll[33];
+  __shared__ int scan_i[33];
+  __shared__ long long red_ll[32];
+  __shared__ double red_d[32];
+  __shared__ int sh_status;
+  __shared__ long long sh_n0, sh_L0, sh_nadd, sh_Ladd;
+  __shared__ double sh_T0, sh_budget, sh_ms;
+  __shared__ int sh_ncand, sh_mstar;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int R = p.R, S = p.S;
+  if (tid == 0) { sh_status = 0; sh_ncand = 0; sh_mstar = 0; }
+  __syncthreads();
+
+  // ---- per-request pass: slot -> request map, validation, protected slot (S0, L128)
+  long long my_L0 = 0, my_n0 = 0;
+  double my_ms = INFINITY;
+  for (int r = tid; r < R; r += blockDim.x) {
+    int b = p.off[r], e = p.off[r + 1];
+    if (b < 0 || e < b || e > S || p.Lsh[r] < 0) { atomicOr(&sh_status, TAPER_STATUS_BAD_LENGTH); continue; }
+    if (e == b) { atomicOr(&sh_status, TAPER_STATUS_EMPTY_REQUEST); continue; }
+    int prot = -1, best = 0;
+    for (int s = b; s < e; ++s) {
+      p.slot_req[s] = r;
+      int l = p.Lloc[s];
+      if (l < 0) atomicOr(&sh_status, TAPER_STATUS_BAD_LENGTH);
+      if (prot < 0 || l < best) { prot = s; best = l; }  // canonical first (Lloc, slot)
+    }
+    if (p.decide) {
+      my_n0 += 1;
+      my_L0 += (long long)p.Lsh[r] + (long long)best;
+      my_ms = fmin(my_ms, p.slack[r]);
+      p.slot_rank[prot] = -1;  // marks the protected slot for the policy pass
+    }
+  }
+  if (p.off[0] != 0 || p.off[R] != S) atomicOr(&sh_status, TAPER_STATUS_BAD_LENGTH);
+
+  if (p.decide) {
+    // ---- S0 aggregates and the slack budget (Sec. 3.3; Alg. 1 L2-4)
+    my_n0 = warp_sum_ll(my_n0);
+    my_L0 = warp_sum_ll(my_L0);
+    my_ms = warp_min_d(my_ms);
+    if (lane == 0) { red_ll[warp] = my_L0; red_d[warp] = my_ms; scan_ll[warp] = my_n0; }
+    __syncthreads();
+    if (tid == 0) {
+      long long n0 = 0, L0 = 0;
+      double ms = INFINITY;
+      for (int w = 0; w < 32; ++w) { n0 += scan_ll[w]; L0 += red_ll[w]; ms = fmin(ms, red_d[w]); }
+      double T0 = T_eval(p.a, p.b, p.c, n0, L0);
+      double budget = T0;
+      if (n0 > 0) {
+        double residual = __dsub_rn(ms, T0);
+        double B = residual > 0.0 ? residual : 0.0;
+        budget = __dadd_rn(T0, __dmul_rn(p.rho, B));
+      }
+      if (p.kind == TAPER_POLICY_GREEDY && p.c < __dmul_rn(budget, 0x1p-46))
+        atomicOr(&sh_status, TAPER_STATUS_PRECISION);
+      sh_n0 = n0; sh_L0 = L0; sh_T0 = T0; sh_budget = budget; sh_ms = ms;
+      sh_nadd = 0; sh_Ladd = 0;
+    }
+    __syncthreads();
+    if (sh_status & TAPER_STATUS_BAD_LENGTH) {
+      // outputs undefined; keep memory-safe defaults
+      for (int s = tid; s < S; s += blockDim.x) p.slot_admitted[s] = 0;
+      __syncthreads();
+    } else {
+      // ---- policy pass: which opportunistic slots join the step
+      int n_keys = 1;
+      while (n_keys < S) n_keys <<= 1;
+      const bool sorted_policy = p.kind == TAPER_POLICY_CAP || p.kind == TAPER_POLICY_GREEDY;
+      long long my_nadd = 0, my_Ladd = 0;
+      for (int s = tid; s < n_keys; s += blockDim.x) {
+        unsigned long long key = ~0ull;
+        if (s < S) {
+          int r = p.slot_req[s];
+          bool prot = p.slot_rank[s] == -1;
+          bool active = r >= 0 && r < R;
+          uint8_t adm = prot ? 1 : 0;
+          if (active && !prot) {
+            long long dL = (long long)p.Lsh[r] + (long long)p.Lloc[s];
+            if (p.kind == TAPER_POLICY_EAGER) {
+              adm = 1; my_nadd += 1; my_Ladd += dL;
+            } else if (p.kind == TAPER_POLICY_CAP) {
+              key = ((unsigned long long)r << 43) | ((unsigned long long)p.Lloc[s] << 12) |
+                    (unsigned long long)s;
+            } else if (p.kind == TAPER_POLICY_GREEDY) {
+              key = ((unsigned long long)dL << 24) | ((unsigned long long)r << 12) |
+                    (unsigned long long)s;
+              atomicAdd(&sh_ncand, 1);
+            }
+          }
+          p.slot_admitted[s] = adm;
+        }
+        if (sorted_policy) keys[s] = key;
+      }
+      __syncthreads();
+      if (sorted_policy) {
+        bitonic_sort(keys, n_keys);
+        if (p.kind == TAPER_POLICY_CAP) {
+          // canonical rank among r's non-protected slots -> admit the first cap-1
+          for (int i = tid; i < S; i += blockDim.x) {
+            unsigned long long k = keys[i];
+            if (k == ~0ull) continue;
+            int r = int(k >> 43), s = int(k & 0xFFF);
+            // non-protected slots of r occupy a contiguous run; rank within it:
+            int first = i;
+            while (first > 0 && keys[first - 1] != ~0ull && int(keys[first - 1] >> 43) == r) --first;
+            if (i - first < p.cap - 1) {
+              p.slot_admitted[s] = 1;
+              my_nadd += 1;
+              my_Ladd += (long long)p.Lsh[r] + (long long)p.Lloc[s];
+            }
+          }
+        } else {
+          // GREEDY: inclusive prefix sums of dL over the sorted candidates
+          const int ncand = sh_ncand;
+          long long v[kPerThread];
+#pragma unroll
+          for (int k = 0; k < kPerThread; ++k) {
+            int i = tid * kPerThread + k;
+            v[k] = (i < ncand) ? (long long)(keys[i] >> 24) : 0;
+          }
+          long long ex[kPerThread];
+#pragma unroll
+          for (int k = 0; k < kPerThread; ++k) ex[k] = v[k];
+          block_exscan4<long long>(ex, scan_ll);
+          int my_feasible = 0;
+#pragma unroll
+          for (int k = 0; k < kPerThread; ++k) {
+            int i = tid * kPerThread + k;  // candidate position; m = i + 1 admitted
+            if (i < ncand) {
+              long long Sm = ex[k] + v[k];
+              double Tm = T_eval(p.a, p.b, p.c, sh_n0 + i + 1, sh_L0 + Sm);
+              if (Tm <= sh_budget) {
+                my_feasible += 1;
+                int s = int(keys[i] & 0xFFF);
+                p.slot_admitted[s] = 1;  // feasible set is a prefix (T monotone in m)
+              }
+            }
+          }
+          int tot = my_feasible;
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, d);
+          if (lane == 0) atomicAdd(&sh_mstar, tot);
+          __syncthreads();
+          const int mstar = sh_mstar;
+#pragma unroll
+          for (int k = 0; k < kPerThread; ++k) {
+            int i = tid * kPerThread + k;
+            if (mstar > 0 && i == mstar - 1) { sh_nadd = mstar; sh_Ladd = ex[k] + v[k]; }
+          }
+          my_nadd = 0; my_Ladd = 0;
+        }
+      }
+      if (p.kind != TAPER_POLICY_GREEDY) {
+        my_nadd = warp_sum_ll(my_nadd);
+        my_Ladd = warp_sum_ll(my_Ladd);
+        if (lane == 0) {
+          atomicAdd(reinterpret_cast<unsigned long long *>(&sh_nadd), (unsigned long long)my_nadd);
+          atomicAdd(reinterpret_cast<unsigned long long *>(&sh_Ladd), (unsigned long long)my_Ladd);
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      double TS = T_eval(p.a, p.b, p.c, sh_n0 + sh_nadd, sh_L0 + sh_Ladd);
+      p.diag[0] = sh_T0;
+      p.diag[1] = sh_budget;
+      p.diag[2] = TS;
+      p.diag[3] = __dsub_rn(TS, sh_T0);  // Sec. 2.3 branch externality E_t(k)
+      p.diag[4] = sh_ms;
+    }
+    __syncthreads();
+  } else {
+    __syncthreads();
+  }
+
+  // ---- work list (A5): per-request widths, chunk counts and CSR offsets
+  int w_loc[kPerThread], nc_loc[kPerThread], cs_loc[kPerThread];
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) {
+    int r = tid * kPerThread + k;
+    int w = 0, nc = 0;
+    if (r < R) {
+      int b = p.off[r], e = p.off[r + 1];
+      if (!(sh_status & TAPER_STATUS_BAD_LENGTH)) {
+        for (int s = b; s < e; ++s) w += p.slot_admitted[s] ? 1 : 0;
+        if (w > 0 && p.Lsh[r] > 0) nc = (p.Lsh[r] + kChunk - 1) / kChunk;
+      }
+      p.req_width[r] = w;
+    }
+    w_loc[k] = w; nc_loc[k] = nc; cs_loc[k] = w * nc;
+  }
+  int tot_w = block_exscan4<int>(w_loc, scan_i);
+  int tot_nc = block_exscan4<int>(nc_loc, scan_i);
+  int tot_cs = block_exscan4<int>(cs_loc, scan_i);
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) {
+    int r = tid * kPerThread + k;
+    if (r < R) {
+      p.req_adm_off[r] = w_loc[k];
+      p.req_chunk_off[r] = nc_loc[k];
+      p.req_part_off[r] = cs_loc[k];
+    }
+  }
+  if (tid == 0) {
+    p.req_adm_off[R] = tot_w;
+    p.req_chunk_off[R] = tot_nc;
+    p.req_part_off[R] = tot_cs;
+  }
+  __syncthreads();
+  // admitted slots of each request in ascending slot order; rank j of each slot
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) {
+    int r = tid * kPerThread + k;
+    if (r < R && !(sh_status & TAPER_STATUS_BAD_LENGTH)) {
+      int j = 0, base = w_loc[k];
+      for (int s = p.off[r]; s < p.off[r + 1]; ++s) {
+        if (p.slot_admitted[s]) { p.adm_by_req[base + j] = s; p.slot_rank[s] = j; ++j; }
+        else p.slot_rank[s] = -2;
+      }
+    }
+  }
+  // adm_list: ascending slot index
+  int f[kPerThread];
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) {
+    int s = tid * kPerThread + k;
+    f[k] = (s < S && !(sh_status & TAPER_STATUS_BAD_LENGTH)) ? p.slot_admitted[s] : 0;
+  }
+  int fl[kPerThread];
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) fl[k] = f[k];
+  int n_adm = block_exscan4<int>(fl, scan_i);
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) {
+    int s = tid * kPerThread + k;
+    if (s < S && f[k]) p.adm_list[fl[k]] = s;
+  }
+  if (tid == 0) {
+    int st = sh_status;
+    int n_rc = tot_nc;
+    if ((long long)tot_cs > p.cap_cs) { st |= TAPER_STATUS_WORK_OVERFLOW; n_rc = 0; }
+    if (st & TAPER_STATUS_BAD_LENGTH) { n_rc = 0; n_adm = 0; }
+    p.hdr[0] = n_rc;
+    p.hdr[1] = tot_cs;
+    p.hdr[2] = n_adm;
+    p.hdr[3] = int(p.cap_cs > 0x7fffffff ? 0x7fffffff : p.cap_cs);
+    p.hdr[4] = p.h_local;
+    *p.n_adm = n_adm;
+    if (p.decide) *p.status = st;
+    else atomicOr(p.status, st);
+  }
+}
+
+}  // namespace taper
+
+// ---------------------------------------------------------------------- host side
+#include "host_common.h"
+
+using namespace taper;
+
+static int launch_admit(const taper_batch *batch, const taper_latency_model *model,
+                        const taper_policy *policy, const taper_admission *out, int32_t h_local,
+                        void *ws, size_t ws_bytes, void *stream, int decide) {
+  if (!batch || !out || !ws) return fail(TAPER_ERR_ARG, "null batch/admission/workspace");
+  const int R = batch->n_req, S = batch->n_slot;
+  if (R < 0 || S < 0) return fail(TAPER_ERR_ARG, "negative n_req/n_slot");
+  if (R > kMaxSlots || S > kMaxSlots) return fail(TAPER_ERR_CAPACITY, "R or S exceeds TAPER_MAX_SLOTS");
+  if (h_local < 1 || h_local > 8) return fail(TAPER_ERR_ARG, "h_local must be in [1, 8]");
+  if (!batch->req_slot_off || (R > 0 && !batch->req_shared_len) ||
+      (S > 0 && !batch->slot_local_len) || (decide && R > 0 && !batch->req_slack_ms))
+    return fail(TAPER_ERR_ARG, "null batch array");
+  if ((R > 0 && !out->req_width) || (S > 0 && (!out->slot_admitted || !out->adm_list)) ||
+      !out->n_adm || !out->status || (decide && !out->diag))
+    return fail(TAPER_ERR_ARG, "null admission output");
+  AdmitParams p{};
+  if (decide) {
+    if (!model || !policy) return fail(TAPER_ERR_ARG, "null model/policy");
+    if (!(policy->rho > 0.0 && policy->rho <= 1.0)) return fail(TAPER_ERR_RHO, "rho must be in (0, 1]");
+    if (!(model->b > 0.0 && model->c > 0.0 && model->a >= 0.0))
+      return fail(TAPER_ERR_NONMONOTONE, "latency model needs a >= 0, b > 0, c > 0");
+    if (policy->kind < TAPER_POLICY_OFF || policy->kind > TAPER_POLICY_GREEDY)
+      return fail(TAPER_ERR_ARG, "unknown policy kind");
+    if (policy->kind == TAPER_POLICY_CAP && policy->cap < 1) return fail(TAPER_ERR_ARG, "cap must be >= 1");
+    if (policy->marginal_utility)
+      return fail(TAPER_ERR_UNSUPPORTED, "only linear utility is implemented on the device");
+    p.a = model->a; p.b = model->b; p.c = model->c; p.rho = policy->rho;
+    p.kind = policy->kind; p.cap = policy->cap;
+  }
+  WsLayout L = ws_layout(R, S);
+  if (ws_bytes < L.fixed) return fail(TAPER_ERR_CAPACITY, "workspace smaller than the fixed part");
+  char *w = static_cast<char *>(ws);
+  p.R = R; p.S = S;
+  p.Lsh = batch->req_shared_len; p.off = batch->req_slot_off; p.Lloc = batch->slot_local_len;
+  p.slack = batch->req_slack_ms;
+  p.decide = decide;
+  p.req_width = out->req_width; p.slot_admitted = out->slot_admitted;
+  p.adm_list = out->adm_list; p.n_adm = out->n_adm; p.diag = out->diag; p.status = out->status;
+  p.hdr = reinterpret_cast<int32_t *>(w + L.hdr);
+  p.slot_req = reinterpret_cast<int32_t *>(w + L.slot_req);
+  p.slot_rank = reinterpret_cast<int32_t *>(w + L.slot_rank);
+  p.req_chunk_off = reinterpret_cast<int32_t *>(w + L.req_chunk_off);
+  p.req_part_off = reinterpret_cast<int32_t *>(w + L.req_part_off);
+  p.req_adm_off = reinterpret_cast<int32_t *>(w + L.req_adm_off);
+  p.adm_by_req = reinterpret_cast<int32_t *>(w + L.adm_by_req);
+  p.cap_cs = ws_cap_cs(ws_bytes, R, S, h_local);
+  p.h_local = h_local;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (S > 0) {
+    cudaError_t e = cudaMemsetAsync(p.slot_req, 0xff, sizeof(int32_t) * S, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p.slot_rank, 0, sizeof(int32_t) * S, st);
+    if (e != cudaSuccess) return fail_cuda(e, "memset workspace");
+  }
+  admit_kernel<<<1, kAdmitThreads, 0, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail_cuda(e, "admit_kernel launch");
+  set_launches(1);
+  return TAPER_OK;
+}
+
+extern "C" int taper_admit(const taper_batch *batch, const taper_latency_model *model,
+                           const taper_policy *policy, const taper_admission *out,
+                           int32_t h_local, void *workspace, size_t workspace_bytes,
+                           void *stream) {
+  return launch_admit(batch, model, policy, out, h_local, workspace, workspace_bytes, stream, 1);
+}
+
+extern "C" int taper_build_work(const taper_batch *batch, const taper_admission *adm,
+                                int32_t h_local, void *workspace, size_t workspace_bytes,
+                                void *stream) {
+  return launch_admit(batch, nullptr, nullptr, adm, h_local, workspace, workspace_bytes, stream, 0);
+}

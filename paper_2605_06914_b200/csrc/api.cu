@@ -1,0 +1,60 @@
+// api.cu -- host helpers of the C ABI: errors, status strings, workspace sizing.
+#include <cstring>
+
+#include "host_common.h"
+#include "taper_internal.cuh"
+
+namespace taper {
+static thread_local char g_last_error[512] = "";
+static thread_local int g_launches = 0;
+
+int fail(int code, const char *msg) {
+  std::snprintf(g_last_error, sizeof g_last_error, "%s", msg);
+  return code;
+}
+int fail_cuda(cudaError_t e, const char *what) {
+  std::snprintf(g_last_error, sizeof g_last_error, "%s: %s", what, cudaGetErrorString(e));
+  return TAPER_ERR_CUDA;
+}
+void set_launches(int n) { g_launches = n; }
+void add_launches(int n) { g_launches += n; }
+}  // namespace taper
+
+extern "C" const char *taper_last_error(void) { return taper::g_last_error; }
+extern "C" int taper_last_launch_count(void) { return taper::g_launches; }
+
+extern "C" const char *taper_status_string(int code) {
+  switch (code) {
+    case TAPER_OK: return "ok";
+    case TAPER_ERR_ARG: return "invalid argument";
+    case TAPER_ERR_RHO: return "rho outside (0, 1]";
+    case TAPER_ERR_NONMONOTONE: return "latency model not monotone (need a >= 0, b > 0, c > 0)";
+    case TAPER_ERR_CAPACITY: return "capacity exceeded (slots, page size or workspace)";
+    case TAPER_ERR_CUDA: return "CUDA error";
+    case TAPER_ERR_UNSUPPORTED: return "unsupported (non-linear utility on device)";
+    default: break;
+  }
+  if (code > 0) {
+    static thread_local char buf[256];
+    buf[0] = 0;
+    if (code & TAPER_STATUS_EMPTY_REQUEST) std::strcat(buf, "empty-request ");
+    if (code & TAPER_STATUS_BAD_LENGTH) std::strcat(buf, "bad-length ");
+    if (code & TAPER_STATUS_PRECISION) std::strcat(buf, "fp64-precision ");
+    if (code & TAPER_STATUS_WORK_OVERFLOW) std::strcat(buf, "work-overflow ");
+    return buf;
+  }
+  return "unknown error";
+}
+
+extern "C" int taper_workspace_size(int32_t n_req, int32_t n_slot, int32_t h_local,
+                                    int64_t max_chunk_slots, size_t *bytes) {
+  if (!bytes || n_req < 0 || n_slot < 0 || max_chunk_slots < 0 || h_local < 1 || h_local > 8)
+    return taper::fail(TAPER_ERR_ARG, "bad workspace_size arguments");
+  if (n_req > taper::kMaxSlots || n_slot > taper::kMaxSlots)
+    return taper::fail(TAPER_ERR_CAPACITY, "R or S exceeds TAPER_MAX_SLOTS");
+  taper::WsLayout L = taper::ws_layout(n_req, n_slot);
+  // partial rows: lse + o for 8 rows per (chunk-slot, head), plus alignment slack
+  size_t part = size_t(max_chunk_slots) * h_local * taper::kPartBytesPerCsHead;
+  *bytes = L.fixed + 512 + part + 512;
+  return TAPER_OK;
+}

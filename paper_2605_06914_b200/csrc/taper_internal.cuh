@@ -1,0 +1,221 @@
+// taper_internal.cuh -- shared definitions of the CUDA path (sm_100a only).
+// Workspace layout, work-list encoding and the inline-PTX wrappers for mbarrier,
+// TMA (cp.async.bulk.tensor), tcgen05 (MMA / TMEM) used by the kernels.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/taper.h"
+
+namespace taper {
+
+constexpr int kHeadDim = TAPER_HEAD_DIM;
+constexpr int kGroup = TAPER_GQA_GROUP;
+constexpr int kChunk = TAPER_CHUNK_TOKENS;
+constexpr int kMaxSlots = TAPER_MAX_SLOTS;
+
+// ------------------------------------------------------------------ workspace layout
+// hdr[0] = n_rc    : number of (request, chunk) pairs with a non-empty shared chunk
+// hdr[1] = n_cs    : sum_r w_r * nchunk_r  (chunk-slots)
+// hdr[2] = n_adm   : admitted slots
+// hdr[3] = cap_cs  : chunk-slot capacity of the partial buffers (for this h_local)
+// hdr[4] = h_local
+struct WsLayout {
+  size_t hdr, slot_req, slot_rank, req_chunk_off, req_part_off, req_adm_off, adm_by_req,
+      part_lse, part_o, fixed;
+};
+
+__host__ __device__ inline size_t ws_align(size_t x) { return (x + 255) & ~size_t(255); }
+
+__host__ __device__ inline WsLayout ws_layout(int R, int S) {
+  WsLayout w;
+  size_t o = 0;
+  w.hdr = o;           o = ws_align(o + 16 * sizeof(int32_t));
+  w.slot_req = o;      o = ws_align(o + size_t(S) * sizeof(int32_t));
+  w.slot_rank = o;     o = ws_align(o + size_t(S) * sizeof(int32_t));
+  w.req_chunk_off = o; o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
+  w.req_part_off = o;  o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
+  w.req_adm_off = o;   o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
+  w.adm_by_req = o;    o = ws_align(o + size_t(S) * sizeof(int32_t));
+  w.fixed = o;
+  w.part_lse = o;  // sized at run time from the workspace bytes
+  w.part_o = o;
+  return w;
+}
+
+// bytes of partial storage per chunk-slot (8 rows x 128 fp32 + 8 lse) per KV head
+constexpr size_t kPartBytesPerCsHead = size_t(kGroup) * (kHeadDim + 1) * sizeof(float);
+
+__host__ __device__ inline int64_t ws_cap_cs(size_t bytes, int R, int S, int h_local) {
+  WsLayout w = ws_layout(R, S);
+  if (bytes < w.fixed + 512) return 0;
+  return int64_t((bytes - w.fixed - 512) / (kPartBytesPerCsHead * size_t(h_local)));
+}
+
+// part_lse then part_o, each indexed by partial row
+//   prow = ((cs * h_local + g) * 8 + qh)
+__host__ __device__ inline void ws_partials(size_t bytes, int R, int S, int h_local,
+                                            size_t *lse_off, size_t *o_off) {
+  WsLayout w = ws_layout(R, S);
+  int64_t cap = ws_cap_cs(bytes, R, S, h_local);
+  *lse_off = w.fixed;
+  *o_off = ws_align(w.fixed + size_t(cap) * h_local * kGroup * sizeof(float));
+}
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Bounded wait: a lost arrival traps (error 700-class) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > (1ll << 35)) __trap();  // ~17 s at 2 GHz
+  }
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// TMA: 4-D tiled load global -> shared, completion on an mbarrier (transaction bytes).
+__device__ __forceinline__ void tma_load_4d(void *smem_dst, const void *tmap, uint64_t *bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const void *tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+
+// ---- tcgen05 (5th-gen tensor cores, TMEM accumulators)
+template <int kCols>
+__device__ __forceinline__ void tmem_alloc(uint32_t *smem_slot) {  // whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(smem_slot)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+template <int kCols>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {  // whole warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T (kind::f16, bf16 inputs, fp32 accumulate)
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+#define TAPER_R4(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3])
+// 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : TAPER_R4(0), TAPER_R4(4), TAPER_R4(8), TAPER_R4(12), TAPER_R4(16), TAPER_R4(20),
+        TAPER_R4(24), TAPER_R4(28)
+      : "r"(taddr));
+}
+#undef TAPER_R4
+#define TAPER_W4(i) "r"(v[i]), "r"(v[i + 1]), "r"(v[i + 2]), "r"(v[i + 3])
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+          taddr),
+      TAPER_W4(0), TAPER_W4(4), TAPER_W4(8), TAPER_W4(12), TAPER_W4(16), TAPER_W4(20),
+      TAPER_W4(24), TAPER_W4(28)
+      : "memory");
+}
+#undef TAPER_W4
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version bit.
+//   K-major : rows of 128 B (64 bf16 of K), 8-row atoms of 1024 B, SBO = atom stride.
+//   MN-major: K-rows of 128 B (64 bf16 of MN), LBO = stride between 64-wide MN blocks,
+//             SBO = stride between 8-row K groups.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t lbo_bytes,
+                                                    uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // descriptor version (sm_100)
+  d |= uint64_t(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, dense.
+__host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N, bool a_mn_major,
+                                                       bool b_mn_major) {
+  return (1u << 4)                           // D format fp32
+         | (1u << 7)                         // A bf16
+         | (1u << 10)                        // B bf16
+         | (uint32_t(a_mn_major) << 15)      // A major
+         | (uint32_t(b_mn_major) << 16)      // B major
+         | (uint32_t(N >> 3) << 17)          // N / 8
+         | (uint32_t(M >> 4) << 24);         // M / 16
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+}  // namespace taper

@@ -1,0 +1,244 @@
+"""Thin ctypes binding of libtaper.so (include/taper.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels of
+``csrc/``.  There is no CPU or PyTorch fallback -- if the library is missing the
+import of this module raises.  Function names mirror the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("TAPER_LIB", os.path.join(_HERE, "libtaper.so"))  # TAPER_LIB: dev builds
+
+TAPER_OK = 0
+TAPER_POLICY_OFF, TAPER_POLICY_CAP, TAPER_POLICY_EAGER, TAPER_POLICY_GREEDY = 0, 1, 2, 3
+POLICY = {"off": 0, "cap": 1, "eager": 2, "taper": 3, "greedy": 3}
+TAPER_STATUS_EMPTY_REQUEST, TAPER_STATUS_BAD_LENGTH = 1, 2
+TAPER_STATUS_PRECISION, TAPER_STATUS_WORK_OVERFLOW = 4, 8
+TAPER_MAX_SLOTS = 4096
+TAPER_CHUNK_TOKENS = 1024
+EXPORTS = ("taper_workspace_size", "taper_admit", "taper_build_work", "taper_decode_attention",
+           "taper_status_string", "taper_last_error", "taper_last_launch_count",
+           "taper_set_profile_events")
+
+_vp = ctypes.c_void_p
+
+
+class _Model(ctypes.Structure):
+    _fields_ = [("a", ctypes.c_double), ("b", ctypes.c_double), ("c", ctypes.c_double)]
+
+
+class _Policy(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("cap", ctypes.c_int32), ("rho", ctypes.c_double),
+                ("marginal_utility", _vp)]
+
+
+class _Batch(ctypes.Structure):
+    _fields_ = [("n_req", ctypes.c_int32), ("n_slot", ctypes.c_int32),
+                ("req_shared_len", _vp), ("req_slot_off", _vp), ("req_slack_ms", _vp),
+                ("slot_local_len", _vp)]
+
+
+class _Admission(ctypes.Structure):
+    _fields_ = [("req_width", _vp), ("slot_admitted", _vp), ("adm_list", _vp), ("n_adm", _vp),
+                ("diag", _vp), ("status", _vp)]
+
+
+class _KV(ctypes.Structure):
+    _fields_ = [("k_pages", _vp), ("v_pages", _vp), ("num_pages", ctypes.c_int32),
+                ("page_size", ctypes.c_int32), ("h_local", ctypes.c_int32),
+                ("req_page_off", _vp), ("req_pages", _vp), ("slot_page_off", _vp),
+                ("slot_pages", _vp)]
+
+
+def load_library() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; "
+                           "g.build()'` (nvcc, sm_100a).  There is no fallback path.")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    lib.taper_workspace_size.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int64, P(ctypes.c_size_t)]
+    lib.taper_admit.argtypes = [P(_Batch), P(_Model), P(_Policy), P(_Admission), ctypes.c_int32,
+                                _vp, ctypes.c_size_t, _vp]
+    lib.taper_build_work.argtypes = [P(_Batch), P(_Admission), ctypes.c_int32, _vp,
+                                     ctypes.c_size_t, _vp]
+    lib.taper_decode_attention.argtypes = [P(_Batch), P(_Admission), P(_KV), _vp, _vp, _vp,
+                                           ctypes.c_float, _vp, ctypes.c_size_t, _vp]
+    lib.taper_status_string.restype = ctypes.c_char_p
+    lib.taper_status_string.argtypes = [ctypes.c_int]
+    lib.taper_last_error.restype = ctypes.c_char_p
+    lib.taper_last_launch_count.restype = ctypes.c_int
+    lib.taper_set_profile_events.restype = ctypes.c_int
+    lib.taper_set_profile_events.argtypes = [_vp, ctypes.c_int]
+    for name in ("taper_workspace_size", "taper_admit", "taper_build_work",
+                 "taper_decode_attention"):
+        getattr(lib, name).restype = ctypes.c_int
+    return lib
+
+
+_lib = load_library()
+
+
+class TaperError(RuntimeError):
+    pass
+
+
+def _check(code: int, what: str):
+    if code != TAPER_OK:
+        raise TaperError(f"{what}: {_lib.taper_status_string(code).decode()} "
+                         f"({_lib.taper_last_error().decode()})")
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def taper_status_string(code: int) -> str:
+    return _lib.taper_status_string(code).decode()
+
+
+def taper_last_launch_count() -> int:
+    return _lib.taper_last_launch_count()
+
+
+def taper_set_profile_events(events) -> None:
+    """events: three torch.cuda.Event (created with enable_timing) or None."""
+    if events is None:
+        _check(_lib.taper_set_profile_events(None, 0), "taper_set_profile_events")
+        return
+    arr = (_vp * 3)(*[e.cuda_event for e in events])
+    _check(_lib.taper_set_profile_events(arr, 3), "taper_set_profile_events")
+
+
+# ------------------------------------------------------------------ device-side containers
+@dataclass
+class DeviceBatch:
+    """taper_batch: device copies of the SoA batch state."""
+    req_shared_len: torch.Tensor  # int32 [R]
+    req_slot_off: torch.Tensor    # int32 [R+1]
+    req_slack_ms: torch.Tensor    # float64 [R]
+    slot_local_len: torch.Tensor  # int32 [S]
+
+    @property
+    def n_req(self):
+        return self.req_shared_len.numel()
+
+    @property
+    def n_slot(self):
+        return self.slot_local_len.numel()
+
+    @classmethod
+    def from_host(cls, b, device="cuda") -> "DeviceBatch":
+        t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(device=device, dtype=dt)
+        return cls(t(b.req_shared_len, torch.int32), t(b.req_slot_off, torch.int32),
+                   t(b.req_slack_ms, torch.float64), t(b.slot_local_len, torch.int32))
+
+    def c(self) -> _Batch:
+        return _Batch(self.n_req, self.n_slot, _ptr(self.req_shared_len), _ptr(self.req_slot_off),
+                      _ptr(self.req_slack_ms), _ptr(self.slot_local_len))
+
+
+@dataclass
+class DeviceAdmission:
+    """taper_admission: caller-allocated admission outputs."""
+    req_width: torch.Tensor
+    slot_admitted: torch.Tensor
+    adm_list: torch.Tensor
+    n_adm: torch.Tensor
+    diag: torch.Tensor
+    status: torch.Tensor
+
+    @classmethod
+    def empty(cls, n_req, n_slot, device="cuda") -> "DeviceAdmission":
+        z = lambda n, dt: torch.zeros(max(n, 1), dtype=dt, device=device)
+        return cls(z(n_req, torch.int32), z(n_slot, torch.uint8), z(n_slot, torch.int32),
+                   z(1, torch.int32), z(5, torch.float64), z(1, torch.int32))
+
+    def c(self) -> _Admission:
+        return _Admission(_ptr(self.req_width), _ptr(self.slot_admitted), _ptr(self.adm_list),
+                          _ptr(self.n_adm), _ptr(self.diag), _ptr(self.status))
+
+
+@dataclass
+class DeviceKV:
+    """taper_kv: one layer's K/V page pools plus the page tables."""
+    k_pages: torch.Tensor  # bf16 [num_pages, h_local, page, 128]
+    v_pages: torch.Tensor
+    req_page_off: torch.Tensor
+    req_pages: torch.Tensor
+    slot_page_off: torch.Tensor
+    slot_pages: torch.Tensor
+
+    def c(self) -> _KV:
+        n, h, ps, d = self.k_pages.shape
+        return _KV(_ptr(self.k_pages), _ptr(self.v_pages), n, ps, h, _ptr(self.req_page_off),
+                   _ptr(self.req_pages), _ptr(self.slot_page_off), _ptr(self.slot_pages))
+
+
+def page_tables_to_device(layout, device="cuda"):
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32)).to(device)
+    pad = lambda a: a if len(a) else np.zeros(1, np.int32)
+    return (t(layout.req_page_off), t(pad(layout.req_pages)), t(layout.slot_page_off),
+            t(pad(layout.slot_pages)))
+
+
+def max_chunk_slots(req_shared_len, req_slot_off) -> int:
+    """Eager-case bound on sum_r w_r * ceil(Lsh_r / 1024) for taper_workspace_size."""
+    lsh = np.asarray(req_shared_len, np.int64)
+    off = np.asarray(req_slot_off, np.int64)
+    return int(((off[1:] - off[:-1]) * ((lsh + TAPER_CHUNK_TOKENS - 1) // TAPER_CHUNK_TOKENS)).sum())
+
+
+# ------------------------------------------------------------------ C-ABI calls
+def taper_workspace_size(n_req: int, n_slot: int, h_local: int, max_chunk_slots: int) -> int:
+    out = ctypes.c_size_t(0)
+    _check(_lib.taper_workspace_size(n_req, n_slot, h_local, max_chunk_slots, ctypes.byref(out)),
+           "taper_workspace_size")
+    return out.value
+
+
+def taper_admit(batch: DeviceBatch, model, policy: str = "taper", rho: float = 0.8,
+                adm: DeviceAdmission = None, h_local: int = 8, workspace: torch.Tensor = None,
+                cap: int = 2, stream=None) -> DeviceAdmission:
+    a, b, c = (float(x) for x in model)
+    kind = POLICY[policy] if isinstance(policy, str) else int(policy)
+    bc, ac = batch.c(), adm.c()
+    _check(_lib.taper_admit(ctypes.byref(bc), ctypes.byref(_Model(a, b, c)),
+                            ctypes.byref(_Policy(kind, cap, rho, None)), ctypes.byref(ac),
+                            h_local, _ptr(workspace), workspace.numel() * workspace.element_size(),
+                            _stream(stream)), "taper_admit")
+    return adm
+
+
+def taper_build_work(batch: DeviceBatch, adm: DeviceAdmission, h_local: int,
+                     workspace: torch.Tensor, stream=None):
+    bc, ac = batch.c(), adm.c()
+    _check(_lib.taper_build_work(ctypes.byref(bc), ctypes.byref(ac), h_local, _ptr(workspace),
+                                 workspace.numel() * workspace.element_size(), _stream(stream)),
+           "taper_build_work")
+
+
+def taper_decode_attention(batch: DeviceBatch, adm: DeviceAdmission, kv: DeviceKV,
+                           q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None,
+                           scale: float, workspace: torch.Tensor, stream=None):
+    assert q.dtype == torch.bfloat16 and out.dtype == torch.bfloat16
+    assert q.is_contiguous() and out.is_contiguous()
+    bc, ac, kc = batch.c(), adm.c(), kv.c()
+    _check(_lib.taper_decode_attention(ctypes.byref(bc), ctypes.byref(ac), ctypes.byref(kc),
+                                       _ptr(q), _ptr(out), _ptr(lse), float(scale),
+                                       _ptr(workspace),
+                                       workspace.numel() * workspace.element_size(),
+                                       _stream(stream)), "taper_decode_attention")

@@ -1,0 +1,43 @@
+"""The C-ABI library loads and exports every symbol include/taper.h declares (CPU-only:
+no compute calls), and the host-side validation paths that need no device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "taper.h")).read()
+    return sorted(set(re.findall(r"TAPER_API\s+[\w\s\*]+?\b(taper_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for n in ("taper_admit", "taper_decode_attention", "taper_build_work", "taper_workspace_size",
+              "taper_status_string"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2605_06914_b200 import build
+    lib_path = build.build()
+    lib = ctypes.CDLL(lib_path)
+    for n in _declared():
+        assert hasattr(lib, n), n
+    from paper_2605_06914_b200 import taper as T
+    assert set(T.EXPORTS) == set(_declared())
+
+
+def test_host_validation_without_gpu():
+    from paper_2605_06914_b200 import taper as T
+    assert T.taper_workspace_size(64, 192, 8, 768) > 768 * 8 * 8 * 129 * 4
+    with pytest.raises(T.TaperError):
+        T.taper_workspace_size(5000, 10, 8, 1)
+    with pytest.raises(T.TaperError):
+        T.taper_workspace_size(10, 10, 9, 1)
+    assert "monotone" in T.taper_status_string(-3)
+    assert "precision" in T.taper_status_string(4)
+    assert T.max_chunk_slots([4096, 1, 0], [0, 3, 4, 6]) == 3 * 4 + 1 + 0
