@@ -52,7 +52,9 @@ def gather_outputs(out_local: torch.Tensor, gathered: torch.Tensor | None = None
         return out_local.unsqueeze(0)
     if gathered is None:
         gathered = out_local.new_empty((world,) + tuple(out_local.shape))
-    dist.all_gather_into_tensor(gathered, out_local.contiguous(), group=group)
+    # concatenated [G*S, ...] view: the form both NCCL and gloo accept
+    dist.all_gather_into_tensor(gathered.view(-1, *out_local.shape[1:]), out_local.contiguous(),
+                                group=group)
     return gathered
 
 

@@ -205,3 +205,89 @@ def plant_sink(k_pages, q, batch: Batch, layout: Layout, gain: float = 32.0):
             qq = q[off[r]:off[r + 1], g * group:(g + 1) * group].float().reshape(-1, q.shape[2])
             mean = qq.mean(0)
             k_pages[page, g, 0] = (gain * mean / mean.norm().clamp_min(1e-6)).to(torch.bfloat16)
+
+
+class TraceReplay:
+    """Config 4: 1000 decode steps of the C2 shape with branch progression.
+
+    Workload dynamics only (no admission, no latency model): the caller supplies the
+    admitted-slot mask of each step (from whichever admission it is testing) and this
+    class advances the state:
+      * every admitted slot generates one token (serial: shared context +1; branch: +1);
+      * a branch reaching its target length (~U{32..512}) completes and leaves the ready
+        set; when every branch of a phase completed, the request enters a reduce stretch
+        (serial) whose context is P (+) H (+) all branches in canonical order (P104-107),
+        lasting U{16..128} tokens, then with probability 0.5 opens a new parallel phase
+        (Table-4 fanout, each branch starting with 1 local token) or stays serial.
+    ``slack_x(step)`` gives the regime schedule of SURVEY Sec. 8(d): x ~ U[1.2, 2] for
+    steps 0-399 (low load), U[-0.5, 0.25] for 400-649 (high), U[0.25, 0.75] after.
+    """
+
+    def __init__(self, seed=0):
+        self.rng = np.random.default_rng(seed)
+        b = config_batch("c2", seed=seed)
+        self.lsh = b.req_shared_len.astype(np.int64).tolist()
+        off = b.req_slot_off
+        self.branches = []   # per request: list of [local_len, target] (empty = serial)
+        self.serial_left = []
+        for r in range(b.n_req):
+            if b.req_serial[r]:
+                self.branches.append([])
+                self.serial_left.append(None)  # serial forever
+            else:
+                self.branches.append([[int(b.slot_local_len[s]),
+                                       int(self.rng.integers(max(32, b.slot_local_len[s] + 1), 513))]
+                                      for s in range(off[r], off[r + 1])])
+                self.serial_left.append(0)
+        self.step_idx = 0
+
+    def slack_x(self, step=None):
+        step = self.step_idx if step is None else step
+        if step < 400:
+            return float(self.rng.uniform(1.2, 2.0))
+        if step < 650:
+            return float(self.rng.uniform(-0.5, 0.25))
+        return float(self.rng.uniform(0.25, 0.75))
+
+    def batch(self, slack_min_ms=0.0) -> Batch:
+        fan, loc = [], []
+        for r, br in enumerate(self.branches):
+            if br:
+                fan.append(len(br))
+                loc += [l for l, _ in br]
+            else:
+                fan.append(1)
+                loc.append(0)
+        return make_batch(self.lsh, fan, loc, slack_min_ms, 20.0, rng=self.rng)
+
+    def advance(self, slot_admitted):
+        s = 0
+        for r, br in enumerate(self.branches):
+            if not br:
+                if slot_admitted[s]:
+                    self.lsh[r] += 1
+                    if self.serial_left[r] is not None and self.serial_left[r] > 0:
+                        self.serial_left[r] -= 1
+                        if self.serial_left[r] == 0 and self.rng.random() < 0.5:
+                            n = int(sample_fanout(self.rng, 1)[0])
+                            self.branches[r] = [[1, int(self.rng.integers(32, 513))]
+                                                for _ in range(n)]
+                s += 1
+                continue
+            done = []
+            for i in range(len(br)):
+                if slot_admitted[s + i]:
+                    br[i][0] += 1
+                    if br[i][0] >= br[i][1]:
+                        done.append(i)
+            s += len(br)
+            if done:
+                self._finished = getattr(self, "_finished", {})
+                fin = self._finished.setdefault(r, [])
+                fin += [br[i][0] for i in done]
+                self.branches[r] = [x for i, x in enumerate(br) if i not in done]
+                if not self.branches[r]:
+                    # reduce phase: context = prefix (+) all completed branches
+                    self.lsh[r] += sum(self._finished.pop(r))
+                    self.serial_left[r] = int(self.rng.integers(16, 129))
+        self.step_idx += 1
