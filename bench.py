@@ -75,7 +75,7 @@ def algorithmic_bytes(batch, adm_mask, h):
     kv_sh = 512 * h * sh_tok
     kv_loc = 512 * h * loc_tok
     q_bytes = n_adm * 8 * h * 128 * 2
-    return {"shared_kernel": kv_sh + q_bytes, "local_kernel": kv_loc + q_bytes,
+    return {"attend_kernel": kv_sh + kv_loc + q_bytes, "merge_kernel": q_bytes,
             "layer": kv_sh + kv_loc + 2 * q_bytes, "kv_shared": kv_sh, "kv_local": kv_loc,
             "noncascade_layer": 512 * h * int((batch.req_shared_len.astype(np.int64)[
                 np.searchsorted(off, np.flatnonzero(adm_mask), side="right") - 1]).sum())
@@ -248,8 +248,8 @@ def run_ours(args):
     # slack relative to the GPU-computed T0 / T_eager (the product computes T, not bench)
     db = T.DeviceBatch.from_host(batch, dev)
     adm = T.DeviceAdmission.empty(R, S, dev)
-    ws = torch.empty(T.taper_workspace_size(R, S, h, T.max_chunk_slots(batch.req_shared_len,
-                                                                       batch.req_slot_off)),
+    ws = torch.empty(T.taper_workspace_size(R, S, h, T.max_chunk_slots(batch.req_shared_len, batch.req_slot_off,
+                                                     batch.slot_local_len)),
                      dtype=torch.uint8, device=dev)
     T.taper_admit(db, MODEL, "off", RHO, adm, h, ws)
     T0 = float(adm.diag[0].item())
@@ -347,7 +347,7 @@ def run_ours(args):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    sh_gbs = by["shared_kernel"] / (sh_avg * 1e-3) / 1e9
+    sh_gbs = by["attend_kernel"] / (sh_avg * 1e-3) / 1e9
     attn_gbs = by["layer"] / ((sh_avg + lo_avg) * 1e-3) / 1e9
     step_gbs = G * L * by["layer"] / (ms_per_step * 1e-3) / 1e9  # whole job, all ranks
 
@@ -382,14 +382,14 @@ def run_ours(args):
             "attn_frac_of_8tbs_spec": attn_gbs / 8000.0,
             "bytes_per_layer_per_gpu": by["layer"],
             "noncascade_bytes_per_layer_per_gpu": by["noncascade_layer"],
-            "kernel_us": {"shared_prefix": sh_avg * 1e3, "local_merge": lo_avg * 1e3,
+            "kernel_us": {"attend": sh_avg * 1e3, "merge": lo_avg * 1e3,
                           "admit_and_collectives_per_step":
                               ms_per_step * 1e3 - L * (sh_avg + lo_avg) * 1e3},
             "roofline": {"bound": "hbm", "achieved": sh_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": sh_gbs / hbm_peak, "traffic": None,
-                         "kernel": "shared_prefix_kernel",
+                         "kernel": "attend_kernel",
                          "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                         "bytes_per_launch": by["shared_kernel"]},
+                         "bytes_per_launch": by["attend_kernel"]},
             "gpu_launches": launches[0] * args.steps,
             "clocks": clocks,
             "e2e": e2e,

@@ -32,8 +32,8 @@ struct AdmitParams {
   int32_t *adm_list, *n_adm;
   double *diag;
   int32_t *status;
-  int32_t *hdr, *slot_req, *slot_rank, *req_chunk_off, *req_part_off, *req_adm_off,
-      *adm_by_req;
+  int32_t *hdr, *slot_req, *slot_rank, *req_chunk_off, *req_loc_off, *req_part_off,
+      *req_adm_off, *adm_by_req;
   int64_t cap_cs;
   int h_local;
 };
@@ -288,24 +288,30 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     __syncthreads();
   }
 
-  // ---- work list (A5): per-request widths, chunk counts and CSR offsets
-  int w_loc[kPerThread], nc_loc[kPerThread], cs_loc[kPerThread];
+  // ---- work list (A5): per-request widths, item counts and CSR offsets.
+  // Shared items: ceil(Lsh / 1024) prefix chunks.  Local items: the admitted branches'
+  // local tiles (64 tokens, never mixing branches) in groups of kLocalItemTiles.
+  int w_loc[kPerThread], nc_loc[kPerThread], nl_loc[kPerThread], cs_loc[kPerThread];
 #pragma unroll
   for (int k = 0; k < kPerThread; ++k) {
     int r = tid * kPerThread + k;
-    int w = 0, nc = 0;
+    int w = 0, nc = 0, nl = 0;
     if (r < R) {
       int b = p.off[r], e = p.off[r + 1];
       if (!(sh_status & TAPER_STATUS_BAD_LENGTH)) {
-        for (int s = b; s < e; ++s) w += p.slot_admitted[s] ? 1 : 0;
+        int lt = 0;
+        for (int s = b; s < e; ++s)
+          if (p.slot_admitted[s]) { w += 1; lt += (p.Lloc[s] + kTileTokens - 1) / kTileTokens; }
         if (w > 0 && p.Lsh[r] > 0) nc = (p.Lsh[r] + kChunk - 1) / kChunk;
+        nl = (lt + kLocalItemTiles - 1) / kLocalItemTiles;
       }
       p.req_width[r] = w;
     }
-    w_loc[k] = w; nc_loc[k] = nc; cs_loc[k] = w * nc;
+    w_loc[k] = w; nc_loc[k] = nc; nl_loc[k] = nl; cs_loc[k] = w * (nc + nl);
   }
   int tot_w = block_exscan4<int>(w_loc, scan_i);
   int tot_nc = block_exscan4<int>(nc_loc, scan_i);
+  int tot_nl = block_exscan4<int>(nl_loc, scan_i);
   int tot_cs = block_exscan4<int>(cs_loc, scan_i);
 #pragma unroll
   for (int k = 0; k < kPerThread; ++k) {
@@ -313,12 +319,14 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     if (r < R) {
       p.req_adm_off[r] = w_loc[k];
       p.req_chunk_off[r] = nc_loc[k];
+      p.req_loc_off[r] = nl_loc[k];
       p.req_part_off[r] = cs_loc[k];
     }
   }
   if (tid == 0) {
     p.req_adm_off[R] = tot_w;
     p.req_chunk_off[R] = tot_nc;
+    p.req_loc_off[R] = tot_nl;
     p.req_part_off[R] = tot_cs;
   }
   __syncthreads();
@@ -352,10 +360,11 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
   }
   if (tid == 0) {
     int st = sh_status;
-    int n_rc = tot_nc;
-    if ((long long)tot_cs > p.cap_cs) { st |= TAPER_STATUS_WORK_OVERFLOW; n_rc = 0; }
-    if (st & TAPER_STATUS_BAD_LENGTH) { n_rc = 0; n_adm = 0; }
+    int n_rc = tot_nc, n_rl = tot_nl;
+    if ((long long)tot_cs > p.cap_cs) { st |= TAPER_STATUS_WORK_OVERFLOW; n_rc = 0; n_rl = 0; n_adm = 0; }
+    if (st & TAPER_STATUS_BAD_LENGTH) { n_rc = 0; n_rl = 0; n_adm = 0; }
     p.hdr[0] = n_rc;
+    p.hdr[5] = n_rl;
     p.hdr[1] = tot_cs;
     p.hdr[2] = n_adm;
     p.hdr[3] = int(p.cap_cs > 0x7fffffff ? 0x7fffffff : p.cap_cs);
@@ -415,6 +424,7 @@ static int launch_admit(const taper_batch *batch, const taper_latency_model *mod
   p.slot_rank = reinterpret_cast<int32_t *>(w + L.slot_rank);
   p.req_chunk_off = reinterpret_cast<int32_t *>(w + L.req_chunk_off);
   p.req_part_off = reinterpret_cast<int32_t *>(w + L.req_part_off);
+  p.req_loc_off = reinterpret_cast<int32_t *>(w + L.req_loc_off);
   p.req_adm_off = reinterpret_cast<int32_t *>(w + L.req_adm_off);
   p.adm_by_req = reinterpret_cast<int32_t *>(w + L.adm_by_req);
   p.cap_cs = ws_cap_cs(ws_bytes, R, S, h_local);

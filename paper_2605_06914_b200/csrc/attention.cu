@@ -3,25 +3,28 @@
 // Sec. 3.1: branch i of a parallel phase attends to
 //     P (+) H (+) h_i (+) y_{i,<t}
 // and "a backend with paged or radix-tree KV caches can serve all branches from a single
-// set of prefix blocks".  The kernels below exploit exactly that:
+// set of prefix blocks".  Two kernels:
 //
-//  A6  shared_prefix_kernel (tcgen05 + TMA, one persistent CTA per SM)
-//      work item = (request r, local KV head g, 1024-token chunk c of P (+) H).
-//      The w_r admitted branches x 8 GQA query heads are stacked into one M = 128 MMA
-//      operand (rows = 8 * w_r <= 128), and every K/V page of the chunk is brought into
-//      shared memory by TMA ONCE and contracted against all stacked rows:
-//          S = Q_stack K^T  (tcgen05.mma, M=128, N=64 tokens, K=128, fp32 in TMEM)
-//          online softmax in registers (one TMEM lane = one query row per thread)
-//          O += P V         (tcgen05.mma, M=128, N=128, K=64 tokens, P bf16 from SMEM)
-//      -> normalised partial (o, lse) per stacked row and chunk.
-//  A7+A8 local_merge_kernel (CUDA cores)
-//      per admitted slot s and local KV head g: 8 query rows over the branch-local
-//      segment h_i (+) y_i -- lane-per-token QK with 16-byte loads, warp-shuffle
-//      softmax, coalesced PV -- then the log-sum-exp merge of the shared-chunk partials
-//      and the local partial into bf16 out[s, 8g:8g+8, :].
+//  A6+A7  attend_kernel (tcgen05 + TMA, one persistent CTA per SM)
+//     Work items of one request r and local KV head g, all sharing the same stacked query
+//     operand Q_stack = [8 GQA heads] x [w_r admitted branches] (rows = 8 w_r <= 128):
+//       * shared item : one 1024-token chunk of P (+) H -- every page read ONCE from HBM
+//                       and contracted against all stacked rows (the cascade);
+//       * local item  : up to 16 64-token tiles of the branches' own segments h_i (+) y_i,
+//                       each tile masked to the 8 rows of the branch that owns it.
+//     Per 64-token tile:  S = Q_stack K^T (tcgen05.mma, A = Q in TMEM, B = K via TMA in
+//     SMEM, fp32 S in TMEM) -> online softmax (one TMEM lane per row) -> P = hi + lo bf16
+//     written back into the S columns of TMEM -> O += P V (tcgen05.mma, A = P in TMEM,
+//     B = V straight from the TMA tile as an MN-major operand).  When <= 32 (<= 64) rows
+//     are live, Q_stack is replicated into 4 (2) TMEM lane quadrants and each copy owns a
+//     16 (32)-token slice of every tile (split-K inside the CTA, PV lanes masked per copy),
+//     so the softmax work is spread over all four SM sub-partitions; the copies are merged
+//     in the epilogue.  Output: a normalised partial (o, lse) per stacked row and item.
+//  A8     merge_kernel: per admitted slot and KV head, log-sum-exp merge of its partials
+//     (prefix chunks in order, then local items) into bf16 out[s, 8g:8g+8, :].
 //
-// Chunk boundaries depend only on the prefix length, and each row's arithmetic does not
-// depend on its position in the stacked operand, so a slot's output does not depend on
+// Item boundaries depend only on segment lengths, and a stacked row's arithmetic does not
+// depend on which other rows share the operand, so a slot's output does not depend on
 // which siblings are co-admitted (Lemma 1; tests/test_gpu_attention.py).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -33,37 +36,27 @@
 
 namespace taper {
 
-constexpr int kTile = 64;      // tokens per pipeline stage
-constexpr int kStages = 4;     // TMA ring depth (4 x 32 KB in flight per SM)
-constexpr int kRowsMax = 128;  // MMA M; 8 * w_r <= 128
-constexpr int kKVStageBytes = 4 * 8192;             // K[d0:64], K[d64:128], V[..], V[..]
-constexpr int kOffQ = kStages * kKVStageBytes;      // 131072
-constexpr int kQBytes = 2 * kRowsMax * 128;         // two 64-column SW128 atoms
-constexpr int kOffP = kOffQ + kQBytes;              // 163840
-constexpr int kPBytes = kRowsMax * 128;             // 128 rows x 64 tokens bf16
-// P precision (DESIGN.md Sec. 9 "P precision"): by default P = hi + lo with both parts
-// bf16 and two PV MMAs, so P carries ~16 mantissa bits (a single bf16 P breaks the
-// 2e-3 / 1e-2 tolerance on peaked softmaxes).  fp16 P against bf16 V is not a legal
-// kind::f16 combination (illegal instruction on sm_100a).  -DTAPER_P_BF16 builds the
-// single-bf16 experiment.
-#if !defined(TAPER_P_BF16)
-#define TAPER_P_SPLIT 1
-constexpr int kPParts = 2;
-#else
-constexpr int kPParts = 1;
-#endif
-constexpr int kOffBar = kOffP + 2 * kPParts * kPBytes;
+constexpr int kTile = kTileTokens;   // 64 tokens per pipeline stage
+constexpr int kStages = 5;           // TMA ring depth (5 x 32 KB in flight per SM)
+constexpr int kKVStageBytes = 4 * 8192;           // K[d0:64], K[d64:128], V[..], V[..]
+constexpr int kOffX = kStages * kKVStageBytes;    // epilogue exchange: 96 rows x 512 B
+constexpr int kXBytes = 96 * 512;
+constexpr int kOffML = kOffX + kXBytes;           // (m, l) of the 128 M-rows
+constexpr int kOffBar = kOffML + 128 * 8;
 constexpr int kSmemUsed = kOffBar + 256;
-constexpr int kSmemBytes = kSmemUsed + 1024;        // + alignment slack
-constexpr int kSharedThreads = 192;                 // warp0 TMA, warp1 MMA, warps2-5 softmax
-constexpr uint32_t kTmemCols = 256;                 // S0 [0,64) S1 [64,128) O [128,256)
+constexpr int kSmemBytes = kSmemUsed + 1024;      // + alignment slack
+constexpr int kAttnThreads = 192;                 // warp0 TMA, warp1 MMA, warps2-5 softmax
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColS = 0;     // S0 / P0 [0, 64), S1 / P1 [64, 128)
+constexpr uint32_t kColO = 128;   // O [128, 256)
+constexpr uint32_t kColQ = 256;   // Q [256, 320): 128 bf16 per row as 64 packed columns
 
 constexpr uint32_t kIdescQK = umma_idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, false, true);
 
-struct SharedParams {
-  const int32_t *Lsh, *req_page_off, *req_pages;
-  const int32_t *hdr, *req_chunk_off, *req_part_off, *req_adm_off, *adm_by_req;
+struct AttnParams {
+  const int32_t *Lsh, *Lloc, *req_page_off, *req_pages, *slot_page_off, *slot_pages;
+  const int32_t *hdr, *req_chunk_off, *req_loc_off, *req_part_off, *req_adm_off, *adm_by_req;
   const __nv_bfloat16 *q;
   float *part_lse, *part_o;
   int R, h_local, page_size;
@@ -71,70 +64,206 @@ struct SharedParams {
 };
 
 struct Item {
-  int r, g, tb, te, nt, w, adm_off, part_base;
+  int r, g, local, w, adm_off, cs0, nt, tb, te, lt0;
 };
 
-__device__ __forceinline__ void decode_item(const SharedParams &p, int it, Item &x) {
-  const int rc = it / p.h_local;
-  x.g = it - rc * p.h_local;
-  int lo = 0, hi = p.R;  // req_chunk_off[lo] <= rc < req_chunk_off[hi]
+__device__ __forceinline__ int upper_search(const int32_t *off, int n, int x) {
+  int lo = 0, hi = n;  // off[lo] <= x < off[hi]
   while (hi - lo > 1) {
     int mid = (lo + hi) >> 1;
-    if (__ldg(p.req_chunk_off + mid) <= rc) lo = mid; else hi = mid;
+    if (__ldg(off + mid) <= x) lo = mid; else hi = mid;
   }
-  x.r = lo;
-  const int c = rc - __ldg(p.req_chunk_off + lo);
-  x.tb = c * kChunk;
-  x.te = min(x.tb + kChunk, __ldg(p.Lsh + lo));
-  x.nt = (x.te - x.tb + kTile - 1) / kTile;
-  x.adm_off = __ldg(p.req_adm_off + lo);
-  x.w = __ldg(p.req_adm_off + lo + 1) - x.adm_off;
-  x.part_base = __ldg(p.req_part_off + lo) + c * x.w;
+  return lo;
 }
 
-// Stage the stacked queries of an item into the SW128 K-major A-operand layout.
-__device__ __forceinline__ void load_q_rows(const SharedParams &p, const Item &x, uint8_t *sQ,
-                                            int row) {
-  if (row >= 8 * x.w) return;
-  const int slot = __ldg(p.adm_by_req + x.adm_off + (row >> 3));
-  const uint4 *src = reinterpret_cast<const uint4 *>(
-      p.q + ((size_t)slot * (kGroup * p.h_local) + x.g * kGroup + (row & 7)) * kHeadDim);
-  uint4 v[16];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) v[c] = __ldg(src + c);
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    const int atom = c >> 3, cc = c & 7;
-    uint8_t *dst = sQ + atom * (kRowsMax * 128) + (row >> 3) * 1024 + (row & 7) * 128 +
-                   ((cc ^ (row & 7)) << 4);
-    *reinterpret_cast<uint4 *>(dst) = v[c];
+__device__ __forceinline__ void decode_item(const AttnParams &p, int it, Item &x) {
+  const int h = p.h_local;
+  const int n_sh = __ldg(p.hdr) * h;
+  int qidx;
+  if (it < n_sh) {
+    const int rc = it / h;
+    x.g = it - rc * h;
+    x.r = upper_search(p.req_chunk_off, p.R, rc);
+    const int c = rc - __ldg(p.req_chunk_off + x.r);
+    x.local = 0;
+    x.tb = c * kChunk;
+    x.te = min(x.tb + kChunk, __ldg(p.Lsh + x.r));
+    x.nt = (x.te - x.tb + kTile - 1) / kTile;
+    x.lt0 = 0;
+    qidx = c;
+  } else {
+    const int it2 = it - n_sh;
+    const int rl = it2 / h;
+    x.g = it2 - rl * h;
+    x.r = upper_search(p.req_loc_off, p.R, rl);
+    const int li = rl - __ldg(p.req_loc_off + x.r);
+    x.local = 1;
+    x.tb = x.te = 0;
+    qidx = (__ldg(p.req_chunk_off + x.r + 1) - __ldg(p.req_chunk_off + x.r)) + li;
+    x.lt0 = li * kLocalItemTiles;
+  }
+  x.adm_off = __ldg(p.req_adm_off + x.r);
+  x.w = __ldg(p.req_adm_off + x.r + 1) - x.adm_off;
+  x.cs0 = __ldg(p.req_part_off + x.r) + qidx * x.w;
+  if (x.local) {
+    int lt = 0;
+    for (int j = 0; j < x.w; ++j)
+      lt += (__ldg(p.Lloc + __ldg(p.adm_by_req + x.adm_off + j)) + kTile - 1) / kTile;
+    x.nt = min(kLocalItemTiles, lt - x.lt0);
   }
 }
 
-__global__ void __launch_bounds__(kSharedThreads, 1)
-    shared_prefix_kernel(const __grid_constant__ CUtensorMap tmK,
-                         const __grid_constant__ CUtensorMap tmV, SharedParams p) {
+struct TileInfo {
+  const int32_t *pages;
+  int tok0, valid, jrow;  // jrow = owning branch (local tiles) or -1 (all rows)
+};
+
+__device__ __forceinline__ TileInfo tile_info(const AttnParams &p, const Item &x, int t) {
+  TileInfo ti;
+  if (!x.local) {
+    ti.pages = p.req_pages + __ldg(p.req_page_off + x.r);
+    ti.tok0 = x.tb + t * kTile;
+    ti.valid = min(kTile, x.te - ti.tok0);
+    ti.jrow = -1;
+  } else {
+    int u = x.lt0 + t, j = 0, s = 0, L = 0;
+    for (; j < x.w; ++j) {
+      s = __ldg(p.adm_by_req + x.adm_off + j);
+      L = __ldg(p.Lloc + s);
+      const int n = (L + kTile - 1) / kTile;
+      if (u < n) break;
+      u -= n;
+    }
+    ti.pages = p.slot_pages + __ldg(p.slot_page_off + s);
+    ti.tok0 = u * kTile;
+    ti.valid = min(kTile, L - ti.tok0);
+    ti.jrow = j;
+  }
+  return ti;
+}
+
+// Replication of the stacked rows over the four TMEM lane quadrants (see header).
+__device__ __forceinline__ int rep_of(int R8) { return R8 <= 32 ? 4 : (R8 <= 64 ? 2 : 1); }
+
+// Stage the (replicated) stacked queries of an item into TMEM columns [kColQ, kColQ+64).
+__device__ __forceinline__ void load_q_tmem(const AttnParams &p, const Item &x, uint32_t tmem,
+                                            uint32_t lane_off, int mrow) {
+  const int R8 = 8 * x.w;
+  const int rpc = 128 / rep_of(R8);
+  const int i = mrow % rpc;
+  uint32_t v[64];
+  if (i < R8) {
+    const int slot = __ldg(p.adm_by_req + x.adm_off + (i >> 3));
+    const uint4 *src = reinterpret_cast<const uint4 *>(
+        p.q + ((size_t)slot * (kGroup * p.h_local) + x.g * kGroup + (i & 7)) * kHeadDim);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const uint4 u = __ldg(src + c);
+      v[4 * c] = u.x; v[4 * c + 1] = u.y; v[4 * c + 2] = u.z; v[4 * c + 3] = u.w;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 64; ++c) v[c] = 0u;
+  }
+  tmem_st_n<64>(tmem + lane_off + kColQ, v);
+}
+
+// One tile of the online softmax for a thread's row.  CW = tokens of the tile owned by
+// this row's copy.  Updates m_run / l_run and writes P (hi, lo) into the row's S columns.
+template <int CW>
+__device__ __forceinline__ void softmax_tile(uint32_t tS, int colbase, int nvalid, bool live,
+                                             bool o_live, float scale_log2, float &m_run,
+                                             float &l_run, uint32_t tO, uint64_t *pv_prev,
+                                             uint32_t pv_prev_parity) {
+  uint32_t s[CW];
+  tmem_ld_n<CW>(tS + colbase, s);
+  tmem_ld_wait();
+  float mx = -INFINITY;
+  if (live) {
+    if (nvalid == CW) {
+#pragma unroll
+      for (int j = 0; j < CW; ++j) mx = fmaxf(mx, __uint_as_float(s[j]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < CW; ++j)
+        if (j < nvalid) mx = fmaxf(mx, __uint_as_float(s[j]));
+    }
+    mx *= scale_log2;
+  }
+  // lazy rescale: only raise the running max when it grows by more than 8 (log2 units)
+  const bool need = live && mx > m_run + 8.f;
+  float alpha = 1.f;
+  if (need) {
+    alpha = ex2(m_run - mx);  // 0 when m_run = -inf
+    l_run *= alpha;
+    m_run = mx;
+  }
+  if (o_live && __any_sync(0xffffffffu, need)) {
+    mbar_wait(pv_prev, pv_prev_parity);  // O *= alpha needs PV(n-1) complete
+    tc_fence_after();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      tmem_ld32(tO + c * 32, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+      tmem_st32(tO + c * 32, o);
+    }
+    tmem_st_wait();
+  }
+  // P = 2^(x - m) split into hi + lo bf16 (DESIGN.md Sec. 6 "P precision"), written back
+  // into this row's S columns in groups of 16 tokens (8 packed columns per part)
+  float lsum = 0.f;
+  const float neg_m = -m_run;
+#pragma unroll
+  for (int g16 = 0; g16 < CW / 16; ++g16) {
+    uint32_t hi[8], lo[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int j = g16 * 8 + jj;
+      float e0 = 0.f, e1 = 0.f;
+      if (live) {
+        if (2 * j < nvalid) e0 = ex2(fmaf(__uint_as_float(s[2 * j]), scale_log2, neg_m));
+        if (2 * j + 1 < nvalid) e1 = ex2(fmaf(__uint_as_float(s[2 * j + 1]), scale_log2, neg_m));
+      }
+      lsum += e0 + e1;
+      const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
+      const float2 f2 = __bfloat1622float2(h2);
+      const __nv_bfloat162 l2 = __floats2bfloat162_rn(e0 - f2.x, e1 - f2.y);
+      hi[jj] = *reinterpret_cast<const uint32_t *>(&h2);
+      lo[jj] = *reinterpret_cast<const uint32_t *>(&l2);
+    }
+    tmem_st8(tS + colbase / 2 + g16 * 8, hi);
+    tmem_st8(tS + 32 + colbase / 2 + g16 * 8, lo);
+  }
+  l_run += lsum;
+  tmem_st_wait();
+}
+
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    attend_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                  AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kOffBar);
-  uint64_t *full = bars;               // [kStages]
-  uint64_t *empty = bars + kStages;    // [kStages]
-  uint64_t *s_full = bars + 2 * kStages;  // [2]
-  uint64_t *p_full = s_full + 2;          // [2]
-  uint64_t *pv_done = p_full + 2;         // [2]
-  uint64_t *q_full = pv_done + 2;
-  uint64_t *o_full = q_full + 1;
-  uint64_t *o_free = o_full + 1;
+  uint64_t *full = bars;                   // [kStages] TMA -> MMA
+  uint64_t *empty = bars + kStages;        // [kStages] MMA -> TMA
+  uint64_t *s_full = bars + 2 * kStages;   // [2] QK done -> softmax
+  uint64_t *p_full = s_full + 2;           // [2] softmax -> PV
+  uint64_t *pv_done = p_full + 2;          // [2] PV done -> softmax (S/P buffer, O)
+  uint64_t *q_full = pv_done + 2;          // softmax (Q staged) -> MMA
+  uint64_t *o_full = q_full + 1;           // last PV of an item -> epilogue
+  uint64_t *o_free = o_full + 1;           // epilogue -> first PV of the next item
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_free + 1);
+  float *xo = reinterpret_cast<float *>(smem + kOffX);
+  float2 *xml = reinterpret_cast<float2 *>(smem + kOffML);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n_items = __ldg(p.hdr) * p.h_local;
+  const int h = p.h_local;
+  const int n_items = (__ldg(p.hdr) + __ldg(p.hdr + 5)) * h;
 
-  // zero the operand buffers once: stale rows must be finite (row independence of MMA)
-  for (int i = tid; i < kOffBar / 16; i += kSharedThreads)
-    reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0, 0, 0, 0);
-  fence_proxy_async_smem();
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
     for (int i = 0; i < 2; ++i) {
@@ -164,17 +293,15 @@ __global__ void __launch_bounds__(kSharedThreads, 1)
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         Item x;
         decode_item(p, it, x);
-        const int32_t *pages = p.req_pages + __ldg(p.req_page_off + x.r);
         for (int t = 0; t < x.nt; ++t) {
+          const TileInfo ti = tile_info(p, x, t);
           mbar_wait(empty + stage, phase ^ 1);
-          const int tok0 = x.tb + t * kTile;
-          const int valid = min(kTile, x.te - tok0);
-          const int n_box = (valid + box_tok - 1) / box_tok;
+          const int n_box = (ti.valid + box_tok - 1) / box_tok;
           mbar_arrive_expect_tx(full + stage, n_box * half_box_bytes * 4);
           uint8_t *st = smem + stage * kKVStageBytes;
           for (int b = 0; b < n_box; ++b) {
-            const int tok = tok0 + b * box_tok;
-            const int page = __ldg(pages + tok / p.page_size);
+            const int tok = ti.tok0 + b * box_tok;
+            const int page = __ldg(ti.pages + tok / p.page_size);
             const int row = tok % p.page_size;
             const int o = b * half_box_bytes;
             tma_load_4d(st + o, &tmK, full + stage, 0, row, x.g, page);
@@ -189,27 +316,37 @@ __global__ void __launch_bounds__(kSharedThreads, 1)
   } else if (warp == 1) {
     // ======================= MMA issuer (single thread) =======================
     if (lane == 0) {
-      const uint32_t sQ = smem_u32(smem + kOffQ);
-      const uint32_t sP0 = smem_u32(smem + kOffP);
       const uint32_t sKV = smem_u32(smem);
-      const uint32_t tO = tmem + 128;
+      const uint32_t tO = tmem + kColO;
+      const uint32_t tQ = tmem + kColQ;
       int stage = 0, prev_stage = 0;
       uint32_t phase = 0;
-      uint32_t n = 0;  // global tile counter
+      uint32_t n = 0;  // global tile counter (S/P double buffer index = n & 1)
       uint32_t item_idx = 0;
+      int rep = 1;
       auto issue_pv = [&](uint32_t m, int st, bool first) {
         mbar_wait(p_full + (m & 1), (m >> 1) & 1);
         if (first) mbar_wait(o_free, (item_idx & 1) ^ 1);
         tc_fence_after();
+        const uint32_t tP = tmem + kColS + (m & 1) * 64;
         const uint32_t vb = sKV + st * kKVStageBytes + 16384;
+        // copy c of the replicated rows owns tokens [c*64/rep, (c+1)*64/rep) of the tile:
+        // its k-steps run with every other copy's TMEM lanes masked off.
+        const int ksteps_per_copy = 4 / rep;
+#pragma unroll 1
+        for (int c = 0; c < rep; ++c) {
+          uint32_t mask[4];
 #pragma unroll
-        for (int part = 0; part < kPParts; ++part) {
-          const uint32_t pa = sP0 + (part * 2 + (m & 1)) * kPBytes;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t a = umma_desc_sw128(pa + kk * 32, 16, 1024);
-            const uint64_t b = umma_desc_sw128(vb + kk * 2048, 8192, 1024);
-            tc_mma_f16(tO, a, b, kIdescPV, (first && part == 0 && kk == 0) ? 0u : 1u);
+          for (int q = 0; q < 4; ++q) mask[q] = (rep == 1 || q / (4 / rep) == c) ? 0u : 0xffffffffu;
+#pragma unroll 1
+          for (int part = 0; part < 2; ++part) {
+#pragma unroll 1
+            for (int k = 0; k < ksteps_per_copy; ++k) {
+              const int kk = c * ksteps_per_copy + k;
+              const uint64_t b = umma_desc_sw128(vb + kk * 2048, 8192, 1024);
+              tc_mma_f16_ts(tO, tP + part * 32 + kk * 8, b, kIdescPV,
+                            (first && part == 0 && k == 0) ? 0u : 1u, mask);
+            }
           }
         }
         tc_commit(empty + st);
@@ -218,18 +355,19 @@ __global__ void __launch_bounds__(kSharedThreads, 1)
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         Item x;
         decode_item(p, it, x);
+        rep = rep_of(8 * x.w);
         mbar_wait(q_full, item_idx & 1);
         tc_fence_after();
         for (int t = 0; t < x.nt; ++t) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
           const uint32_t kb = sKV + stage * kKVStageBytes;
-          const uint32_t tS = tmem + (n & 1) * 64;
+          const uint32_t tS = tmem + kColS + (n & 1) * 64;
+          const uint32_t nomask[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t a = umma_desc_sw128(sQ + (kk >> 2) * (kRowsMax * 128) + (kk & 3) * 32, 16, 1024);
             const uint64_t b = umma_desc_sw128(kb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
-            tc_mma_f16(tS, a, b, kIdescQK, kk > 0 ? 1u : 0u);
+            tc_mma_f16_ts(tS, tQ + kk * 8, b, kIdescQK, kk > 0 ? 1u : 0u, nomask);
           }
           tc_commit(s_full + (n & 1));
           if (t > 0) issue_pv(n - 1, prev_stage, t == 1);
@@ -245,97 +383,48 @@ __global__ void __launch_bounds__(kSharedThreads, 1)
   } else {
     // ======================= softmax / correction / epilogue (128 threads) ===========
     const int wq = warp & 3;            // TMEM lane quadrant of this warp
-    const int row = wq * 32 + lane;     // query row owned by this thread
+    const int mrow = wq * 32 + lane;    // M-row (TMEM lane) owned by this thread
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
-    uint8_t *sQ = smem + kOffQ;
+    const uint32_t tO = tmem + lane_off + kColO;
     uint32_t n = 0, item_idx = 0;
     if (blockIdx.x < n_items) {
       Item x0;
       decode_item(p, blockIdx.x, x0);
-      load_q_rows(p, x0, sQ, row);
-      fence_proxy_async_smem();
+      load_q_tmem(p, x0, tmem, lane_off, mrow);
+      tmem_st_wait();
+      tc_fence_before();
       mbar_arrive(q_full);
     }
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       Item x;
       decode_item(p, it, x);
       const int R8 = 8 * x.w;
-      const bool warp_active = wq * 32 < R8;
+      const int rep = rep_of(R8);
+      const int rpc = 128 / rep, cw = 64 / rep;
+      const int copy = mrow / rpc, i = mrow - copy * rpc;
+      const int colbase = copy * cw;
       float m_run = -INFINITY, l_run = 0.f;
       for (int t = 0; t < x.nt; ++t) {
         const uint32_t sb = n & 1;
+        const TileInfo ti = tile_info(p, x, t);
+        const bool live = i < R8 && (ti.jrow < 0 || (i >> 3) == ti.jrow);
+        const int nvalid = max(0, min(cw, ti.valid - colbase));
         mbar_wait(s_full + sb, (n >> 1) & 1);
         tc_fence_after();
-        if (warp_active) {
-          uint32_t s0[32], s1[32];
-          const uint32_t tS = tmem + lane_off + sb * 64;
-          tmem_ld32(tS, s0);
-          tmem_ld32(tS + 32, s1);
-          tmem_ld_wait();
-          const int valid = min(kTile, x.te - (x.tb + t * kTile));
-          float xs[64];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            xs[j] = j < valid ? __uint_as_float(s0[j]) * p.scale_log2 : -INFINITY;
-            xs[32 + j] = (32 + j) < valid ? __uint_as_float(s1[j]) * p.scale_log2 : -INFINITY;
-          }
-          float mx = xs[0];
-#pragma unroll
-          for (int j = 1; j < 64; ++j) mx = fmaxf(mx, xs[j]);
-          // lazy rescale: keep a stale max unless the row max grew by > 8 (2^8 headroom)
-          const bool need = mx > m_run + 8.f;
-          float alpha = 1.f;
-          if (need) {
-            alpha = ex2(m_run - mx);  // 0 when m_run = -inf
-            l_run *= alpha;
-            m_run = mx;
-          }
-          if (t > 0 && __any_sync(0xffffffffu, need)) {
-            // O *= alpha needs PV(n-1) complete
-            mbar_wait(pv_done + ((n - 1) & 1), ((n - 1) >> 1) & 1);
-            tc_fence_after();
-            const uint32_t tO = tmem + lane_off + 128;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t o[32];
-              tmem_ld32(tO + c * 32, o);
-              tmem_ld_wait();
-#pragma unroll
-              for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-              tmem_st32(tO + c * 32, o);
-            }
-            tmem_st_wait();
-          }
-          // P = 2^(x - m) in bf16; l accumulates the rounded values actually multiplied
-          uint32_t pk[kPParts][32];
-          float lsum = 0.f;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float e0 = ex2(xs[2 * j] - m_run), e1 = ex2(xs[2 * j + 1] - m_run);
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
-            float2 f2 = __bfloat1622float2(h2);
-            pk[0][j] = *reinterpret_cast<uint32_t *>(&h2);
-#if defined(TAPER_P_SPLIT)
-            __nv_bfloat162 l2 = __floats2bfloat162_rn(e0 - f2.x, e1 - f2.y);
-            float2 g2 = __bfloat1622float2(l2);
-            pk[1][j] = *reinterpret_cast<uint32_t *>(&l2);
-            lsum += (f2.x + g2.x) + (f2.y + g2.y);
-#else
-            lsum += f2.x + f2.y;
-#endif
-          }
-          l_run += lsum;
-          if (n >= 2) mbar_wait(pv_done + sb, ((n >> 1) - 1) & 1);  // P[sb] free
-#pragma unroll
-          for (int part = 0; part < kPParts; ++part) {
-            uint8_t *prow = smem + kOffP + (part * 2 + sb) * kPBytes + (row >> 3) * 1024 + (row & 7) * 128;
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              *reinterpret_cast<uint4 *>(prow + ((c ^ (row & 7)) << 4)) =
-                  make_uint4(pk[part][4 * c], pk[part][4 * c + 1], pk[part][4 * c + 2], pk[part][4 * c + 3]);
-          }
-          fence_proxy_async_smem();
-        }
+        // P[sb] aliases S[sb]: PV(n-2) finished reading it before QK(n) was issued.
+        const uint32_t tS = tmem + lane_off + kColS + sb * 64;
+        uint64_t *pv_prev = pv_done + ((n - 1) & 1);
+        const uint32_t pv_par = ((n - 1) >> 1) & 1;
+        const bool o_live = t > 0;
+        if (cw == 16)
+          softmax_tile<16>(tS, colbase, nvalid, live, o_live, p.scale_log2, m_run, l_run, tO,
+                           pv_prev, pv_par);
+        else if (cw == 32)
+          softmax_tile<32>(tS, colbase, nvalid, live, o_live, p.scale_log2, m_run, l_run, tO,
+                           pv_prev, pv_par);
+        else
+          softmax_tile<64>(tS, colbase, nvalid, live, o_live, p.scale_log2, m_run, l_run, tO,
+                           pv_prev, pv_par);
         tc_fence_before();
         mbar_arrive(p_full + sb);
         ++n;
@@ -345,34 +434,68 @@ __global__ void __launch_bounds__(kSharedThreads, 1)
       if (next < n_items) {
         Item xn;
         decode_item(p, next, xn);
-        load_q_rows(p, xn, sQ, row);
-        fence_proxy_async_smem();
+        load_q_tmem(p, xn, tmem, lane_off, mrow);
+        tmem_st_wait();
+        tc_fence_before();
         mbar_arrive(q_full);
       }
-      // epilogue: normalised partial (o, lse) for each live row
+      // ---- epilogue: merge the copies of each stacked row, write the partial (o, lse)
       mbar_wait(o_full, item_idx & 1);
       tc_fence_after();
-      if (warp_active) {
-        const bool live = row < R8;
-        const size_t prow = ((size_t)(x.part_base + (row >> 3)) * p.h_local + x.g) * kGroup + (row & 7);
-        const float inv_l = 1.f / l_run;
-        float4 *dst = reinterpret_cast<float4 *>(p.part_o + prow * kHeadDim);
-        const uint32_t tO = tmem + lane_off + 128;
-#pragma unroll
+      xml[mrow] = make_float2(m_run, l_run);
+      named_bar_sync(1, 128);
+      float M = -INFINITY, L = 0.f;
+      for (int c = 0; c < rep; ++c) M = fmaxf(M, xml[c * rpc + i].x);
+      for (int c = 0; c < rep; ++c) {
+        const float2 ml = xml[c * rpc + i];
+        if (ml.y > 0.f) L += ex2(ml.x - M) * ml.y;
+      }
+      const float f = (L > 0.f && l_run > 0.f) ? ex2(m_run - M) / L : 0.f;
+      const bool out_row = i < R8;
+      const bool warp_out = __any_sync(0xffffffffu, out_row);
+      // copies 1..rep-1 park their scaled rows in SMEM; copy 0 adds them and stores
+      if (warp_out && copy > 0) {
+#pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           uint32_t o[32];
           tmem_ld32(tO + c * 32, o);
           tmem_ld_wait();
-          if (live) {
+          if (out_row) {
+            float4 *xr = reinterpret_cast<float4 *>(xo + ((copy - 1) * rpc + i) * kHeadDim) + c * 8;
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-              dst[c * 8 + j] = make_float4(__uint_as_float(o[4 * j]) * inv_l,
-                                           __uint_as_float(o[4 * j + 1]) * inv_l,
-                                           __uint_as_float(o[4 * j + 2]) * inv_l,
-                                           __uint_as_float(o[4 * j + 3]) * inv_l);
+              xr[j] = make_float4(__uint_as_float(o[4 * j]) * f, __uint_as_float(o[4 * j + 1]) * f,
+                                  __uint_as_float(o[4 * j + 2]) * f,
+                                  __uint_as_float(o[4 * j + 3]) * f);
           }
         }
-        if (live) p.part_lse[prow] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+      }
+      named_bar_sync(1, 128);
+      if (warp_out && copy == 0) {
+        const size_t prow = ((size_t)(x.cs0 + (i >> 3)) * h + x.g) * kGroup + (i & 7);
+        if (out_row)
+          p.part_lse[prow] = L > 0.f ? (M + __log2f(L)) * 0.69314718055994531f : -INFINITY;
+        float4 *d4 = reinterpret_cast<float4 *>(p.part_o + prow * kHeadDim);
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + c * 32, o);
+          tmem_ld_wait();
+          if (out_row) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 a = make_float4(__uint_as_float(o[4 * j]) * f, __uint_as_float(o[4 * j + 1]) * f,
+                                     __uint_as_float(o[4 * j + 2]) * f,
+                                     __uint_as_float(o[4 * j + 3]) * f);
+              for (int cc = 1; cc < rep; ++cc) {
+                const float4 b = reinterpret_cast<const float4 *>(
+                    xo + ((cc - 1) * rpc + i) * kHeadDim)[c * 8 + j];
+                a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+              }
+              d4[c * 8 + j] = a;
+            }
+          }
+        }
       }
       tc_fence_before();
       mbar_arrive(o_free);
@@ -387,176 +510,68 @@ __global__ void __launch_bounds__(kSharedThreads, 1)
   }
 }
 
-// ------------------------------------------------------------------ local + merge
-constexpr int kLocalThreads = 128;
+// ------------------------------------------------------------------ A8: LSE merge
+constexpr int kMergeThreads = 256;  // one warp per (admitted slot, KV head)
 
-struct LocalParams {
-  const int32_t *Lsh, *Lloc, *slot_page_off, *slot_pages;
-  const int32_t *hdr, *slot_req, *slot_rank, *req_chunk_off, *req_part_off, *req_adm_off,
-      *adm_list;
-  const __nv_bfloat16 *q, *k_pages, *v_pages;
+struct MergeParams {
+  const int32_t *hdr, *slot_req, *slot_rank, *req_chunk_off, *req_loc_off, *req_part_off,
+      *req_adm_off, *adm_list;
   const float *part_lse, *part_o;
   __nv_bfloat16 *out;
   float *lse_out;
-  int h_local, page_size;
-  float scale_log2;
+  int h_local;
 };
 
-__device__ __forceinline__ float warp_max(float x) {
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, d));
-  return x;
-}
-__device__ __forceinline__ float warp_sum(float x) {
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
-  return x;
-}
-
-__global__ void __launch_bounds__(kLocalThreads) local_merge_kernel(LocalParams p) {
-  __shared__ __align__(16) float qs[kGroup][kHeadDim];
-  __shared__ __align__(16) float wo[4][kGroup][kHeadDim];
-  __shared__ float wm[4][kGroup], wl[4][kGroup];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+__global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
+  const int lane = threadIdx.x & 31;
   const int h = p.h_local;
   const int n_items = __ldg(p.hdr + 2) * h;
   const int qheads = kGroup * h;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+  const int warps = gridDim.x * (kMergeThreads / 32);
+  for (int it = blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5); it < n_items;
+       it += warps) {
     const int k = it / h, g = it - k * h;
     const int s = __ldg(p.adm_list + k);
     const int r = __ldg(p.slot_req + s);
     const int j = __ldg(p.slot_rank + s);
-    const int adm0 = __ldg(p.req_adm_off + r);
-    const int w = __ldg(p.req_adm_off + r + 1) - adm0;
-    __syncthreads();  // smem reuse across items
-    {
-      const int rr = tid >> 4, d0 = (tid & 15) * 8;
-      const uint4 raw = __ldg(reinterpret_cast<const uint4 *>(
-          p.q + ((size_t)s * qheads + g * kGroup + rr) * kHeadDim + d0));
-      const __nv_bfloat162 *b2 = reinterpret_cast<const __nv_bfloat162 *>(&raw);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float2 f = __bfloat1622float2(b2[i]);
-        qs[rr][d0 + 2 * i] = f.x * p.scale_log2;
-        qs[rr][d0 + 2 * i + 1] = f.y * p.scale_log2;
-      }
-    }
-    __syncthreads();
-    // ---------------- A7: branch-local segment, split over 4 warps
-    const int Ll = __ldg(p.Lloc + s);
-    const int32_t *pages = p.slot_pages + __ldg(p.slot_page_off + s);
-    float m[kGroup], lsum[kGroup], o[kGroup][4];
+    const int w = __ldg(p.req_adm_off + r + 1) - __ldg(p.req_adm_off + r);
+    const int nq = (__ldg(p.req_chunk_off + r + 1) - __ldg(p.req_chunk_off + r)) +
+                   (__ldg(p.req_loc_off + r + 1) - __ldg(p.req_loc_off + r));
+    const int cs_base = __ldg(p.req_part_off + r) + j;
+    float M[kGroup], Z[kGroup], acc[kGroup][4];
 #pragma unroll
     for (int a = 0; a < kGroup; ++a) {
-      m[a] = -INFINITY; lsum[a] = 0.f;
-      o[a][0] = o[a][1] = o[a][2] = o[a][3] = 0.f;
+      M[a] = -INFINITY; Z[a] = 0.f;
+      acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
     }
-    for (int blk = warp; blk * 32 < Ll; blk += 4) {
-      const int t = blk * 32 + lane;
-      const bool valid = t < Ll;
-      float x[kGroup];
-      if (valid) {
-        const int page = __ldg(pages + t / p.page_size);
-        const uint4 *kr = reinterpret_cast<const uint4 *>(
-            p.k_pages + (((size_t)page * h + g) * p.page_size + t % p.page_size) * kHeadDim);
+    for (int q = 0; q < nq; ++q) {
+      const size_t prow0 = ((size_t)(cs_base + q * w) * h + g) * kGroup;
 #pragma unroll
-        for (int a = 0; a < kGroup; ++a) x[a] = 0.f;
-#pragma unroll 4
-        for (int c = 0; c < 16; ++c) {
-          const uint4 raw = __ldg(kr + c);
-          const __nv_bfloat162 *b2 = reinterpret_cast<const __nv_bfloat162 *>(&raw);
-          float kf[8];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float2 f = __bfloat1622float2(b2[i]);
-            kf[2 * i] = f.x; kf[2 * i + 1] = f.y;
-          }
-#pragma unroll
-          for (int a = 0; a < kGroup; ++a) {
-            const float4 q0 = *reinterpret_cast<const float4 *>(&qs[a][c * 8]);
-            const float4 q1 = *reinterpret_cast<const float4 *>(&qs[a][c * 8 + 4]);
-            x[a] += q0.x * kf[0] + q0.y * kf[1] + q0.z * kf[2] + q0.w * kf[3] +
-                    q1.x * kf[4] + q1.y * kf[5] + q1.z * kf[6] + q1.w * kf[7];
-          }
-        }
-      } else {
-#pragma unroll
-        for (int a = 0; a < kGroup; ++a) x[a] = -INFINITY;
-      }
-      float pr[kGroup];
+      for (int a = 0; a < kGroup; ++a)
+        M[a] = fmaxf(M[a], __ldg(p.part_lse + prow0 + a) * 1.4426950408889634f);
+    }
+    for (int q = 0; q < nq; ++q) {
+      const size_t prow0 = ((size_t)(cs_base + q * w) * h + g) * kGroup;
 #pragma unroll
       for (int a = 0; a < kGroup; ++a) {
-        const float mn = fmaxf(m[a], warp_max(x[a]));
-        const float alpha = ex2(m[a] - mn);
-        pr[a] = valid ? ex2(x[a] - mn) : 0.f;
-        lsum[a] = lsum[a] * alpha + pr[a];
-        o[a][0] *= alpha; o[a][1] *= alpha; o[a][2] *= alpha; o[a][3] *= alpha;
-        m[a] = mn;
-      }
-      const int nvalid = min(32, Ll - blk * 32);
-      for (int jj = 0; jj < nvalid; ++jj) {
-        const int tj = blk * 32 + jj;
-        const int page = __ldg(pages + tj / p.page_size);
-        const uint2 raw = __ldg(reinterpret_cast<const uint2 *>(
-            p.v_pages + (((size_t)page * h + g) * p.page_size + tj % p.page_size) * kHeadDim +
-            4 * lane));
-        const __nv_bfloat162 *b2 = reinterpret_cast<const __nv_bfloat162 *>(&raw);
-        const float2 v01 = __bfloat1622float2(b2[0]), v23 = __bfloat1622float2(b2[1]);
-#pragma unroll
-        for (int a = 0; a < kGroup; ++a) {
-          const float pj = __shfl_sync(0xffffffffu, pr[a], jj);
-          o[a][0] += pj * v01.x; o[a][1] += pj * v01.y;
-          o[a][2] += pj * v23.x; o[a][3] += pj * v23.y;
-        }
+        const float l2 = __ldg(p.part_lse + prow0 + a) * 1.4426950408889634f;
+        if (l2 == -INFINITY) continue;
+        const float wgt = ex2(l2 - M[a]);
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(p.part_o + (prow0 + a) * kHeadDim) + lane);
+        acc[a][0] += wgt * v.x; acc[a][1] += wgt * v.y; acc[a][2] += wgt * v.z; acc[a][3] += wgt * v.w;
+        Z[a] += wgt;
       }
     }
 #pragma unroll
     for (int a = 0; a < kGroup; ++a) {
-      const float l = warp_sum(lsum[a]);
-      if (lane == 0) { wm[warp][a] = m[a]; wl[warp][a] = l; }
-      *reinterpret_cast<float4 *>(&wo[warp][a][4 * lane]) = make_float4(o[a][0], o[a][1], o[a][2], o[a][3]);
-    }
-    __syncthreads();
-    // ---------------- A8: log-sum-exp merge (shared chunks in order, then local warps)
-    {
-      const int rr = tid >> 4, d0 = (tid & 15) * 8;
-      const int c0 = __ldg(p.req_chunk_off + r), nch = __ldg(p.req_chunk_off + r + 1) - c0;
-      const int cs0 = __ldg(p.req_part_off + r) + j;
-      float M = -INFINITY;
-      for (int c = 0; c < nch; ++c) {
-        const size_t prow = ((size_t)(cs0 + c * w) * h + g) * kGroup + rr;
-        M = fmaxf(M, __ldg(p.part_lse + prow) * 1.4426950408889634f);
-      }
-#pragma unroll
-      for (int ww = 0; ww < 4; ++ww) if (wl[ww][rr] > 0.f) M = fmaxf(M, wm[ww][rr]);
-      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      float Z = 0.f;
-      for (int c = 0; c < nch; ++c) {
-        const size_t prow = ((size_t)(cs0 + c * w) * h + g) * kGroup + rr;
-        const float wgt = ex2(__ldg(p.part_lse + prow) * 1.4426950408889634f - M);
-        const float4 *src = reinterpret_cast<const float4 *>(p.part_o + prow * kHeadDim + d0);
-        const float4 a0 = __ldg(src), a1 = __ldg(src + 1);
-        acc[0] += wgt * a0.x; acc[1] += wgt * a0.y; acc[2] += wgt * a0.z; acc[3] += wgt * a0.w;
-        acc[4] += wgt * a1.x; acc[5] += wgt * a1.y; acc[6] += wgt * a1.z; acc[7] += wgt * a1.w;
-        Z += wgt;
-      }
-#pragma unroll
-      for (int ww = 0; ww < 4; ++ww) {
-        if (wl[ww][rr] > 0.f) {
-          const float wgt = ex2(wm[ww][rr] - M);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] += wgt * wo[ww][rr][d0 + i];
-          Z += wgt * wl[ww][rr];
-        }
-      }
-      const float invZ = 1.f / Z;
-      __align__(16) __nv_bfloat162 ob[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) ob[i] = __floats2bfloat162_rn(acc[2 * i] * invZ, acc[2 * i + 1] * invZ);
-      *reinterpret_cast<uint4 *>(p.out + ((size_t)s * qheads + g * kGroup + rr) * kHeadDim + d0) =
-          *reinterpret_cast<uint4 *>(ob);
-      if (p.lse_out && (tid & 15) == 0)
-        p.lse_out[(size_t)s * qheads + g * kGroup + rr] = (M + __log2f(Z)) * 0.69314718055994531f;
+      const float inv = 1.f / Z[a];
+      __align__(8) __nv_bfloat162 o2[2];
+      o2[0] = __floats2bfloat162_rn(acc[a][0] * inv, acc[a][1] * inv);
+      o2[1] = __floats2bfloat162_rn(acc[a][2] * inv, acc[a][3] * inv);
+      *reinterpret_cast<uint2 *>(p.out + ((size_t)s * qheads + g * kGroup + a) * kHeadDim + 4 * lane) =
+          *reinterpret_cast<uint2 *>(o2);
+      if (p.lse_out && lane == a)
+        p.lse_out[(size_t)s * qheads + g * kGroup + a] = (M[a] + __log2f(Z[a])) * 0.69314718055994531f;
     }
   }
 }
@@ -648,7 +663,6 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   size_t lse_off, o_off;
   ws_partials(workspace_bytes, R, S, h, &lse_off, &o_off);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const float scale_log2 = scale * 1.4426950408889634f;
 
   CUtensorMap tmK, tmV;
   int rc = make_kv_map(&tmK, kv->k_pages, kv);
@@ -658,61 +672,57 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
 
   static thread_local bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(shared_prefix_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(shared_prefix_kernel)");
+    cudaError_t e = cudaFuncSetAttribute(attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kSmemBytes);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(attend_kernel)");
     attr_set = true;
   }
-  SharedParams sp;
-  sp.Lsh = batch->req_shared_len;
-  sp.req_page_off = kv->req_page_off;
-  sp.req_pages = kv->req_pages;
-  sp.hdr = reinterpret_cast<const int32_t *>(w + L.hdr);
-  sp.req_chunk_off = reinterpret_cast<const int32_t *>(w + L.req_chunk_off);
-  sp.req_part_off = reinterpret_cast<const int32_t *>(w + L.req_part_off);
-  sp.req_adm_off = reinterpret_cast<const int32_t *>(w + L.req_adm_off);
-  sp.adm_by_req = reinterpret_cast<const int32_t *>(w + L.adm_by_req);
-  sp.q = static_cast<const __nv_bfloat16 *>(q);
-  sp.part_lse = reinterpret_cast<float *>(w + lse_off);
-  sp.part_o = reinterpret_cast<float *>(w + o_off);
-  sp.R = R;
-  sp.h_local = h;
-  sp.page_size = kv->page_size;
-  sp.scale_log2 = scale_log2;
+  AttnParams ap;
+  ap.Lsh = batch->req_shared_len;
+  ap.Lloc = batch->slot_local_len;
+  ap.req_page_off = kv->req_page_off;
+  ap.req_pages = kv->req_pages;
+  ap.slot_page_off = kv->slot_page_off;
+  ap.slot_pages = kv->slot_pages;
+  ap.hdr = reinterpret_cast<const int32_t *>(w + L.hdr);
+  ap.req_chunk_off = reinterpret_cast<const int32_t *>(w + L.req_chunk_off);
+  ap.req_loc_off = reinterpret_cast<const int32_t *>(w + L.req_loc_off);
+  ap.req_part_off = reinterpret_cast<const int32_t *>(w + L.req_part_off);
+  ap.req_adm_off = reinterpret_cast<const int32_t *>(w + L.req_adm_off);
+  ap.adm_by_req = reinterpret_cast<const int32_t *>(w + L.adm_by_req);
+  ap.q = static_cast<const __nv_bfloat16 *>(q);
+  ap.part_lse = reinterpret_cast<float *>(w + lse_off);
+  ap.part_o = reinterpret_cast<float *>(w + o_off);
+  ap.R = R;
+  ap.h_local = h;
+  ap.page_size = kv->page_size;
+  ap.scale_log2 = scale * 1.4426950408889634f;
   const int sms = device_sms();
   if (g_prof_ev[0]) cudaEventRecord(g_prof_ev[0], st);
-  shared_prefix_kernel<<<sms, kSharedThreads, kSmemBytes, st>>>(tmK, tmV, sp);
+  attend_kernel<<<sms, kAttnThreads, kSmemBytes, st>>>(tmK, tmV, ap);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail_cuda(e, "shared_prefix_kernel launch");
+  if (e != cudaSuccess) return fail_cuda(e, "attend_kernel launch");
   if (g_prof_ev[1]) cudaEventRecord(g_prof_ev[1], st);
 
-  LocalParams lp;
-  lp.Lsh = batch->req_shared_len;
-  lp.Lloc = batch->slot_local_len;
-  lp.slot_page_off = kv->slot_page_off;
-  lp.slot_pages = kv->slot_pages;
-  lp.hdr = sp.hdr;
-  lp.slot_req = reinterpret_cast<const int32_t *>(w + L.slot_req);
-  lp.slot_rank = reinterpret_cast<const int32_t *>(w + L.slot_rank);
-  lp.req_chunk_off = sp.req_chunk_off;
-  lp.req_part_off = sp.req_part_off;
-  lp.req_adm_off = sp.req_adm_off;
-  lp.adm_list = adm->adm_list;
-  lp.q = sp.q;
-  lp.k_pages = static_cast<const __nv_bfloat16 *>(kv->k_pages);
-  lp.v_pages = static_cast<const __nv_bfloat16 *>(kv->v_pages);
-  lp.part_lse = sp.part_lse;
-  lp.part_o = sp.part_o;
-  lp.out = static_cast<__nv_bfloat16 *>(out);
-  lp.lse_out = lse;
-  lp.h_local = h;
-  lp.page_size = kv->page_size;
-  lp.scale_log2 = scale_log2;
-  int grid = S * h;
+  MergeParams mp;
+  mp.hdr = ap.hdr;
+  mp.slot_req = reinterpret_cast<const int32_t *>(w + L.slot_req);
+  mp.slot_rank = reinterpret_cast<const int32_t *>(w + L.slot_rank);
+  mp.req_chunk_off = ap.req_chunk_off;
+  mp.req_loc_off = ap.req_loc_off;
+  mp.req_part_off = ap.req_part_off;
+  mp.req_adm_off = ap.req_adm_off;
+  mp.adm_list = adm->adm_list;
+  mp.part_lse = ap.part_lse;
+  mp.part_o = ap.part_o;
+  mp.out = static_cast<__nv_bfloat16 *>(out);
+  mp.lse_out = lse;
+  mp.h_local = h;
+  int grid = (S * h + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
   if (grid > sms * 8) grid = sms * 8;
-  local_merge_kernel<<<grid, kLocalThreads, 0, st>>>(lp);
+  merge_kernel<<<grid, kMergeThreads, 0, st>>>(mp);
   e = cudaGetLastError();
-  if (e != cudaSuccess) return fail_cuda(e, "local_merge_kernel launch");
+  if (e != cudaSuccess) return fail_cuda(e, "merge_kernel launch");
   if (g_prof_ev[2]) cudaEventRecord(g_prof_ev[2], st);
   set_launches(2);
   return TAPER_OK;

@@ -14,16 +14,19 @@ constexpr int kHeadDim = TAPER_HEAD_DIM;
 constexpr int kGroup = TAPER_GQA_GROUP;
 constexpr int kChunk = TAPER_CHUNK_TOKENS;
 constexpr int kMaxSlots = TAPER_MAX_SLOTS;
+constexpr int kTileTokens = 64;       // tokens per pipeline tile (one TMA stage)
+constexpr int kLocalItemTiles = 16;   // branch-local tiles per local work item
 
 // ------------------------------------------------------------------ workspace layout
-// hdr[0] = n_rc    : number of (request, chunk) pairs with a non-empty shared chunk
-// hdr[1] = n_cs    : sum_r w_r * nchunk_r  (chunk-slots)
+// hdr[0] = n_rc    : number of (request, prefix chunk) pairs (shared items per KV head)
+// hdr[1] = n_cs    : sum_r w_r * (nchunk_r + nloc_r)  (partial "chunk-slots")
 // hdr[2] = n_adm   : admitted slots
 // hdr[3] = cap_cs  : chunk-slot capacity of the partial buffers (for this h_local)
 // hdr[4] = h_local
+// hdr[5] = n_rl    : number of (request, local item) pairs (local items per KV head)
 struct WsLayout {
-  size_t hdr, slot_req, slot_rank, req_chunk_off, req_part_off, req_adm_off, adm_by_req,
-      part_lse, part_o, fixed;
+  size_t hdr, slot_req, slot_rank, req_chunk_off, req_loc_off, req_part_off, req_adm_off,
+      adm_by_req, part_lse, part_o, fixed;
 };
 
 __host__ __device__ inline size_t ws_align(size_t x) { return (x + 255) & ~size_t(255); }
@@ -35,6 +38,7 @@ __host__ __device__ inline WsLayout ws_layout(int R, int S) {
   w.slot_req = o;      o = ws_align(o + size_t(S) * sizeof(int32_t));
   w.slot_rank = o;     o = ws_align(o + size_t(S) * sizeof(int32_t));
   w.req_chunk_off = o; o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
+  w.req_loc_off = o;   o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
   w.req_part_off = o;  o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
   w.req_adm_off = o;   o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
   w.adm_by_req = o;    o = ws_align(o + size_t(S) * sizeof(int32_t));
@@ -44,7 +48,8 @@ __host__ __device__ inline WsLayout ws_layout(int R, int S) {
   return w;
 }
 
-// bytes of partial storage per chunk-slot (8 rows x 128 fp32 + 8 lse) per KV head
+// bytes of partial storage per chunk-slot (8 rows x 128 fp32 + 8 lse) per KV head;
+// a chunk-slot is one (work item, admitted slot) pair: prefix chunks and local items
 constexpr size_t kPartBytesPerCsHead = size_t(kGroup) * (kHeadDim + 1) * sizeof(float);
 
 __host__ __device__ inline int64_t ws_cap_cs(size_t bytes, int R, int S, int h_local) {
@@ -148,6 +153,20 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t a_desc, uin
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem]^T ("TS": A operand read from tensor memory, K-major,
+// two bf16 per 32-bit column); lanes whose bit is set in `mask` keep their old D.
+__device__ __forceinline__ void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate,
+                                              const uint32_t (&mask)[4]) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(
+          d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(mask[0]), "r"(mask[1]),
+      "r"(mask[2]), "r"(mask[3])
+      : "memory");
+}
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.
 __device__ __forceinline__ void tc_commit(uint64_t *bar) {
   asm volatile(
@@ -178,6 +197,58 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       : "memory");
 }
 #undef TAPER_W4
+// N = 8 / 16 consecutive 32-bit columns per lane (32 lanes of the warp's quadrant)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                   taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),
+               "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15])
+      : "memory");
+}
+// generic N-column helpers built from the fixed-width instructions
+template <int N>
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, uint32_t *v) {
+  if constexpr (N == 16) {
+    tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(v));
+  } else {
+#pragma unroll
+    for (int i = 0; i < N / 32; ++i)
+      tmem_ld32(taddr + 32 * i, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * i));
+  }
+}
+template <int N>
+__device__ __forceinline__ void tmem_st_n(uint32_t taddr, const uint32_t *v) {
+  if constexpr (N == 8) {
+    tmem_st8(taddr, *reinterpret_cast<const uint32_t(*)[8]>(v));
+  } else if constexpr (N == 16) {
+    tmem_st16(taddr, *reinterpret_cast<const uint32_t(*)[16]>(v));
+  } else {
+#pragma unroll
+    for (int i = 0; i < N / 32; ++i)
+      tmem_st32(taddr + 32 * i, *reinterpret_cast<const uint32_t(*)[32]>(v + 32 * i));
+  }
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n_threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n_threads) : "memory");
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }

@@ -195,11 +195,24 @@ def page_tables_to_device(layout, device="cuda"):
             t(pad(layout.slot_pages)))
 
 
-def max_chunk_slots(req_shared_len, req_slot_off) -> int:
-    """Eager-case bound on sum_r w_r * ceil(Lsh_r / 1024) for taper_workspace_size."""
+TAPER_TILE_TOKENS = 64
+TAPER_LOCAL_ITEM_TILES = 16
+
+
+def max_chunk_slots(req_shared_len, req_slot_off, slot_local_len) -> int:
+    """Eager-case bound on sum_r w_r * (prefix chunks + local items) of request r, for
+    taper_workspace_size (prefix chunks of 1024 tokens; local items of up to 16 64-token
+    tiles of the branches' own segments)."""
     lsh = np.asarray(req_shared_len, np.int64)
     off = np.asarray(req_slot_off, np.int64)
-    return int(((off[1:] - off[:-1]) * ((lsh + TAPER_CHUNK_TOKENS - 1) // TAPER_CHUNK_TOKENS)).sum())
+    lloc = np.asarray(slot_local_len, np.int64)
+    n = off[1:] - off[:-1]
+    chunks = (lsh + TAPER_CHUNK_TOKENS - 1) // TAPER_CHUNK_TOKENS
+    tiles = (lloc + TAPER_TILE_TOKENS - 1) // TAPER_TILE_TOKENS
+    lt = np.add.reduceat(tiles, off[:-1]) if len(tiles) else np.zeros(len(n), np.int64)
+    lt = np.where(n > 0, lt, 0)
+    local_items = (lt + TAPER_LOCAL_ITEM_TILES - 1) // TAPER_LOCAL_ITEM_TILES
+    return int((n * (chunks + local_items)).sum())
 
 
 # ------------------------------------------------------------------ C-ABI calls

@@ -11,10 +11,10 @@ timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TA
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --layers 64 \
   --no-e2e --no-cpu-baseline > /dev/null 2> gpurun_out/ncu_launch_$TAG.err; tail -3 gpurun_out/ncu_launch_$TAG.err
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:shared_prefix -s 8 -c 1 \
-  -o gpurun_out/prof_shared_$TAG -f python bench.py --steps 1 --warmup 3 --layers 4 --no-e2e \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:attend_kernel -s 8 -c 1 \
+  -o gpurun_out/prof_attend_$TAG -f python bench.py --steps 1 --warmup 3 --layers 4 --no-e2e \
   --no-cpu-baseline > /dev/null 2> gpurun_out/ncu_full_$TAG.err; tail -3 gpurun_out/ncu_full_$TAG.err
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:local_merge -s 8 -c 1 \
-  -o gpurun_out/prof_local_$TAG -f python bench.py --steps 1 --warmup 3 --layers 4 --no-e2e \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:merge_kernel -s 8 -c 1 \
+  -o gpurun_out/prof_merge_$TAG -f python bench.py --steps 1 --warmup 3 --layers 4 --no-e2e \
   --no-cpu-baseline > /dev/null 2> gpurun_out/ncu_full_local_$TAG.err; tail -3 gpurun_out/ncu_full_local_$TAG.err
 ls -la gpurun_out

@@ -38,7 +38,7 @@ class Case:
         db = T.DeviceBatch.from_host(b, dev)
         adm = T.DeviceAdmission.empty(b.n_req, b.n_slot, dev)
         ws_bytes = T.taper_workspace_size(b.n_req, b.n_slot, h,
-                                          T.max_chunk_slots(b.req_shared_len, b.req_slot_off))
+                                          T.max_chunk_slots(b.req_shared_len, b.req_slot_off, b.slot_local_len))
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         T.taper_admit(db, model, policy, rho, adm, h, ws, cap)
         rpo, rp, spo, sp = T.page_tables_to_device(self.layout, dev)

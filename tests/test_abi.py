@@ -40,4 +40,4 @@ def test_host_validation_without_gpu():
         T.taper_workspace_size(10, 10, 9, 1)
     assert "monotone" in T.taper_status_string(-3)
     assert "precision" in T.taper_status_string(4)
-    assert T.max_chunk_slots([4096, 1, 0], [0, 3, 4, 6]) == 3 * 4 + 1 + 0
+    assert T.max_chunk_slots([4096, 1, 0], [0, 3, 4, 6], [0, 65, 1, 0, 2, 3]) == 3 * (4 + 1) + 1 + 2 * 1

@@ -15,7 +15,7 @@ def _gpu_admit(b, model, policy, rho, cap=2, h=8):
     db = T.DeviceBatch.from_host(b)
     adm = T.DeviceAdmission.empty(b.n_req, b.n_slot)
     ws = torch.empty(T.taper_workspace_size(b.n_req, b.n_slot, h,
-                                            T.max_chunk_slots(b.req_shared_len, b.req_slot_off)),
+                                            T.max_chunk_slots(b.req_shared_len, b.req_slot_off, b.slot_local_len)),
                      dtype=torch.uint8, device="cuda")
     T.taper_admit(db, model, policy, rho, adm, h, ws, cap)
     torch.cuda.synchronize()
