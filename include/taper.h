@@ -168,6 +168,11 @@ TAPER_API int taper_decode_attention(const taper_batch *batch, const taper_admis
  * call's stream (cudaEvent_t handles passed as void*).  NULL disables.  [host]          */
 TAPER_API int taper_set_profile_events(void *const *events, int n_events);
 
+/* Debug hook: when non-NULL, attend_kernel records clock64() timestamps of its pipeline
+ * events (TMA issue, MMA issue/commit, softmax start/end, epilogue) for CTA 0 into
+ * device_buffer[tile * 16 + event] (int64, capacity_tiles * 16 entries).  [host]        */
+TAPER_API int taper_set_trace_buffer(void *device_buffer, int capacity_tiles);
+
 /* Human-readable text for a TAPER_ERR_* code or TAPER_STATUS_* bit set.  [host]        */
 TAPER_API const char *taper_status_string(int code);
 /* Last error message of this thread (detail of the most recent failing call).  [host]  */

@@ -36,6 +36,8 @@ struct AdmitParams {
       *req_adm_off, *adm_by_req;
   int64_t cap_cs;
   int h_local;
+  ItemDesc *items;   // [cap_cs] work items (A5)
+  int4 *ltiles;      // [cap_cs * 16] local tiles {slot, tok0, valid, jrow}
 };
 
 __device__ __forceinline__ double T_eval(double a, double b, double c, long long n,
@@ -342,6 +344,47 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       }
     }
   }
+  __syncthreads();
+  // item and local-tile descriptors (A5): one request per thread
+  const bool fits = (long long)tot_cs <= p.cap_cs;
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) {
+    int r = tid * kPerThread + k;
+    if (r >= R || !fits || (sh_status & TAPER_STATUS_BAD_LENGTH)) continue;
+    const int w = p.req_adm_off[r + 1] - p.req_adm_off[r];
+    if (w == 0) continue;
+    const int adm_off = p.req_adm_off[r];
+    const int nr = p.off[r + 1] - p.off[r];
+    const int rep = (8 * nr <= 32) ? 4 : ((8 * nr <= 64) ? 2 : 1);
+    const int nc = p.req_chunk_off[r + 1] - p.req_chunk_off[r];
+    const int cs_r = p.req_part_off[r];
+    for (int c = 0; c < nc; ++c) {
+      ItemDesc d;
+      d.r = r; d.w = w; d.adm_off = adm_off; d.cs0 = cs_r + c * w;
+      d.tb = c * kChunk; d.te = min(d.tb + kChunk, p.Lsh[r]);
+      d.nt = (d.te - d.tb + kTileTokens - 1) / kTileTokens;
+      d.flags = rep << 1;
+      p.items[p.req_chunk_off[r] + c] = d;
+    }
+    // local tiles of the admitted branches, branch-major, grouped 16 per local item
+    const int l0 = p.req_loc_off[r], nl = p.req_loc_off[r + 1] - l0;
+    int lt = 0;
+    for (int j = 0; j < w; ++j) {
+      const int s = p.adm_by_req[adm_off + j];
+      const int L = p.Lloc[s];
+      for (int t0 = 0; t0 < L; t0 += kTileTokens, ++lt)
+        p.ltiles[(size_t)(l0 + lt / kLocalItemTiles) * kLocalItemTiles + lt % kLocalItemTiles] =
+            make_int4(s, t0, min(kTileTokens, L - t0), j);
+    }
+    for (int li = 0; li < nl; ++li) {
+      ItemDesc d;
+      d.r = r; d.w = w; d.adm_off = adm_off; d.cs0 = cs_r + (nc + li) * w;
+      d.tb = (l0 + li) * kLocalItemTiles; d.te = 0;
+      d.nt = min(kLocalItemTiles, lt - li * kLocalItemTiles);
+      d.flags = 1 | (rep << 1);
+      p.items[tot_nc + l0 + li] = d;
+    }
+  }
   // adm_list: ascending slot index
   int f[kPerThread];
 #pragma unroll
@@ -427,7 +470,10 @@ static int launch_admit(const taper_batch *batch, const taper_latency_model *mod
   p.req_loc_off = reinterpret_cast<int32_t *>(w + L.req_loc_off);
   p.req_adm_off = reinterpret_cast<int32_t *>(w + L.req_adm_off);
   p.adm_by_req = reinterpret_cast<int32_t *>(w + L.adm_by_req);
-  p.cap_cs = ws_cap_cs(ws_bytes, R, S, h_local);
+  WsTables T = ws_tables(ws_bytes, R, S, h_local);
+  p.cap_cs = T.cap_cs;
+  p.items = reinterpret_cast<ItemDesc *>(w + T.items);
+  p.ltiles = reinterpret_cast<int4 *>(w + T.ltiles);
   p.h_local = h_local;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (S > 0) {

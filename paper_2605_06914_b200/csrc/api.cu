@@ -53,8 +53,9 @@ extern "C" int taper_workspace_size(int32_t n_req, int32_t n_slot, int32_t h_loc
   if (n_req > taper::kMaxSlots || n_slot > taper::kMaxSlots)
     return taper::fail(TAPER_ERR_CAPACITY, "R or S exceeds TAPER_MAX_SLOTS");
   taper::WsLayout L = taper::ws_layout(n_req, n_slot);
-  // partial rows: lse + o for 8 rows per (chunk-slot, head), plus alignment slack
-  size_t part = size_t(max_chunk_slots) * h_local * taper::kPartBytesPerCsHead;
-  *bytes = L.fixed + 512 + part + 512;
+  // per chunk-slot: partial rows (8 x (128 + 1) fp32 per head) + work descriptors
+  size_t part = size_t(max_chunk_slots) *
+                (size_t(h_local) * taper::kPartBytesPerCsHead + taper::kWorkBytesPerCs);
+  *bytes = L.fixed + 1024 + part + 2048;
   return TAPER_OK;
 }

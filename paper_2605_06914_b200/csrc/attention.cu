@@ -39,78 +39,55 @@ namespace taper {
 constexpr int kTile = kTileTokens;   // 64 tokens per pipeline stage
 constexpr int kStages = 5;           // TMA ring depth (5 x 32 KB in flight per SM)
 constexpr int kKVStageBytes = 4 * 8192;           // K[d0:64], K[d64:128], V[..], V[..]
-constexpr int kOffX = kStages * kKVStageBytes;    // epilogue exchange: 96 rows x 512 B
-constexpr int kXBytes = 96 * 512;
-constexpr int kOffML = kOffX + kXBytes;           // (m, l) of the 128 M-rows
-constexpr int kOffBar = kOffML + 128 * 8;
+constexpr int kXStride = 132;                     // floats per exchange row (bank padding)
+constexpr int kOffX = kStages * kKVStageBytes;    // epilogue exchange: 96 rows
+constexpr int kXBytes = 96 * kXStride * 4;
+constexpr int kOffML = kOffX + kXBytes;           // (m, l) of the 128 M-rows, 2 buffers
+constexpr int kOffBar = kOffML + 2 * 128 * 8;
 constexpr int kSmemUsed = kOffBar + 256;
 constexpr int kSmemBytes = kSmemUsed + 1024;      // + alignment slack
-constexpr int kAttnThreads = 192;                 // warp0 TMA, warp1 MMA, warps2-5 softmax
+// warp 0: TMA producer; warp 1: MMA issuer; warps 2-5: softmax; warps 6-9: epilogue
+constexpr int kAttnThreads = 320;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0;     // S0 / P0 [0, 64), S1 / P1 [64, 128)
-constexpr uint32_t kColO = 128;   // O [128, 256)
-constexpr uint32_t kColQ = 256;   // Q [256, 320): 128 bf16 per row as 64 packed columns
+constexpr uint32_t kColO = 128;   // O0 [128, 256), O1 [256, 384)
+constexpr uint32_t kColQ = 384;   // Q [384, 448): 128 bf16 per row as 64 packed columns
 
 constexpr uint32_t kIdescQK = umma_idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, false, true);
 
 struct AttnParams {
-  const int32_t *Lsh, *Lloc, *req_page_off, *req_pages, *slot_page_off, *slot_pages;
-  const int32_t *hdr, *req_chunk_off, *req_loc_off, *req_part_off, *req_adm_off, *adm_by_req;
+  const int32_t *slot_page_off, *slot_pages, *req_page_off, *req_pages;
+  const int32_t *hdr, *adm_by_req;
+  const ItemDesc *items;
+  const int4 *ltiles;
   const __nv_bfloat16 *q;
   float *part_lse, *part_o;
-  int R, h_local, page_size;
+  int h_local, page_size;
   float scale_log2;
+  long long *trace;  // debug: pipeline event timestamps of CTA 0 (taper_set_trace_buffer)
+  int trace_cap;
 };
 
-struct Item {
-  int r, g, local, w, adm_off, cs0, nt, tb, te, lt0;
-};
-
-__device__ __forceinline__ int upper_search(const int32_t *off, int n, int x) {
-  int lo = 0, hi = n;  // off[lo] <= x < off[hi]
-  while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (__ldg(off + mid) <= x) lo = mid; else hi = mid;
-  }
-  return lo;
+// Debug trace: event e of tile/item index n -> trace[(n * 16 + e)] = clock64 (CTA 0 only).
+__device__ __forceinline__ void trace_ev(const AttnParams &p, int e, uint32_t n) {
+  if (p.trace != nullptr && blockIdx.x == 0 && int(n) < p.trace_cap)
+    p.trace[(size_t)n * 16 + e] = clock64();
 }
 
+struct Item {
+  int r, g, local, w, adm_off, cs0, nt, tb, te, rep;
+};
+
 __device__ __forceinline__ void decode_item(const AttnParams &p, int it, Item &x) {
-  const int h = p.h_local;
-  const int n_sh = __ldg(p.hdr) * h;
-  int qidx;
-  if (it < n_sh) {
-    const int rc = it / h;
-    x.g = it - rc * h;
-    x.r = upper_search(p.req_chunk_off, p.R, rc);
-    const int c = rc - __ldg(p.req_chunk_off + x.r);
-    x.local = 0;
-    x.tb = c * kChunk;
-    x.te = min(x.tb + kChunk, __ldg(p.Lsh + x.r));
-    x.nt = (x.te - x.tb + kTile - 1) / kTile;
-    x.lt0 = 0;
-    qidx = c;
-  } else {
-    const int it2 = it - n_sh;
-    const int rl = it2 / h;
-    x.g = it2 - rl * h;
-    x.r = upper_search(p.req_loc_off, p.R, rl);
-    const int li = rl - __ldg(p.req_loc_off + x.r);
-    x.local = 1;
-    x.tb = x.te = 0;
-    qidx = (__ldg(p.req_chunk_off + x.r + 1) - __ldg(p.req_chunk_off + x.r)) + li;
-    x.lt0 = li * kLocalItemTiles;
-  }
-  x.adm_off = __ldg(p.req_adm_off + x.r);
-  x.w = __ldg(p.req_adm_off + x.r + 1) - x.adm_off;
-  x.cs0 = __ldg(p.req_part_off + x.r) + qidx * x.w;
-  if (x.local) {
-    int lt = 0;
-    for (int j = 0; j < x.w; ++j)
-      lt += (__ldg(p.Lloc + __ldg(p.adm_by_req + x.adm_off + j)) + kTile - 1) / kTile;
-    x.nt = min(kLocalItemTiles, lt - x.lt0);
-  }
+  const int q = it / p.h_local;
+  x.g = it - q * p.h_local;
+  const int4 a = __ldg(reinterpret_cast<const int4 *>(p.items + q));
+  const int4 b = __ldg(reinterpret_cast<const int4 *>(p.items + q) + 1);
+  x.r = a.x; x.w = a.y; x.adm_off = a.z; x.cs0 = a.w;
+  x.tb = b.x; x.te = b.y; x.nt = b.z;
+  x.local = b.w & 1;
+  x.rep = b.w >> 1;
 }
 
 struct TileInfo {
@@ -126,30 +103,27 @@ __device__ __forceinline__ TileInfo tile_info(const AttnParams &p, const Item &x
     ti.valid = min(kTile, x.te - ti.tok0);
     ti.jrow = -1;
   } else {
-    int u = x.lt0 + t, j = 0, s = 0, L = 0;
-    for (; j < x.w; ++j) {
-      s = __ldg(p.adm_by_req + x.adm_off + j);
-      L = __ldg(p.Lloc + s);
-      const int n = (L + kTile - 1) / kTile;
-      if (u < n) break;
-      u -= n;
-    }
-    ti.pages = p.slot_pages + __ldg(p.slot_page_off + s);
-    ti.tok0 = u * kTile;
-    ti.valid = min(kTile, L - ti.tok0);
-    ti.jrow = j;
+    const int4 lt = __ldg(p.ltiles + x.tb + t);  // {slot, tok0, valid, branch}
+    ti.pages = p.slot_pages + __ldg(p.slot_page_off + lt.x);
+    ti.tok0 = lt.y;
+    ti.valid = lt.z;
+    ti.jrow = lt.w;
   }
   return ti;
 }
 
-// Replication of the stacked rows over the four TMEM lane quadrants (see header).
-__device__ __forceinline__ int rep_of(int R8) { return R8 <= 32 ? 4 : (R8 <= 64 ? 2 : 1); }
+// valid tokens and owning branch of tile t (softmax side: no page lookup)
+__device__ __forceinline__ int2 tile_rows(const AttnParams &p, const Item &x, int t) {
+  if (!x.local) return make_int2(min(kTile, x.te - (x.tb + t * kTile)), -1);
+  const int4 lt = __ldg(p.ltiles + x.tb + t);
+  return make_int2(lt.z, lt.w);
+}
 
 // Stage the (replicated) stacked queries of an item into TMEM columns [kColQ, kColQ+64).
 __device__ __forceinline__ void load_q_tmem(const AttnParams &p, const Item &x, uint32_t tmem,
                                             uint32_t lane_off, int mrow) {
   const int R8 = 8 * x.w;
-  const int rpc = 128 / rep_of(R8);
+  const int rpc = 128 / x.rep;
   const int i = mrow % rpc;
   uint32_t v[64];
   if (i < R8) {
@@ -166,6 +140,52 @@ __device__ __forceinline__ void load_q_tmem(const AttnParams &p, const Item &x, 
     for (int c = 0; c < 64; ++c) v[c] = 0u;
   }
   tmem_st_n<64>(tmem + lane_off + kColQ, v);
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// S[tS] = Q[tQ] * K^T: 8 k-steps of 16 over d = 128 (A = Q from TMEM, B = K tile in SMEM,
+// SW128 K-major: d 0..63 in the first 8 KB box, 64..127 in the second).
+__device__ __forceinline__ void issue_qk(uint32_t tS, uint32_t tQ, uint32_t kb) {
+  const uint32_t nomask[4] = {0u, 0u, 0u, 0u};
+  const uint64_t b0 = umma_desc_sw128(kb, 16, 1024);
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const uint64_t b = b0 + uint64_t((((kk >> 2) * 8192) + (kk & 3) * 32) >> 4);
+    tc_mma_f16_ts(tS, tQ + kk * 8, b, kIdescQK, kk > 0 ? 1u : 0u, nomask);
+  }
+}
+
+// O[tO] += P[tP] * V: P = hi (columns 0..31) + lo (32..63), 4 k-steps of 16 tokens;
+// B = V tile as an MN-major SW128 operand (d 0..63 / 64..127 boxes 8 KB apart).  With REP
+// replicated row copies, copy c owns tokens [c*64/REP, (c+1)*64/REP): its k-steps run
+// with the other copies' TMEM lanes masked off.
+template <int REP>
+__device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t vb, bool first) {
+  const uint64_t b0 = umma_desc_sw128(vb, 8192, 1024);
+  constexpr int KPC = 4 / REP;
+#pragma unroll
+  for (int c = 0; c < REP; ++c) {
+    uint32_t mask[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mask[q] = (REP == 1 || q / (4 / REP) == c) ? 0u : 0xffffffffu;
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+#pragma unroll
+      for (int k = 0; k < KPC; ++k) {
+        const int kk = c * KPC + k;
+        const uint64_t b = b0 + uint64_t((kk * 2048) >> 4);
+        tc_mma_f16_ts(tO, tP + part * 32 + kk * 8, b, kIdescPV,
+                      (first && part == 0 && k == 0) ? 0u : 1u, mask);
+      }
+    }
+  }
 }
 
 // One tile of the online softmax for a thread's row.  CW = tokens of the tile owned by
@@ -245,18 +265,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     attend_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                              ~uintptr_t(1023));
+  // 1024-B alignment (SW128) by pointer arithmetic on the shared array, so the compiler
+  // keeps the shared address space (LDS/STS instead of generic loads)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kOffBar);
   uint64_t *full = bars;                   // [kStages] TMA -> MMA
   uint64_t *empty = bars + kStages;        // [kStages] MMA -> TMA
   uint64_t *s_full = bars + 2 * kStages;   // [2] QK done -> softmax
   uint64_t *p_full = s_full + 2;           // [2] softmax -> PV
-  uint64_t *pv_done = p_full + 2;          // [2] PV done -> softmax (S/P buffer, O)
+  uint64_t *pv_done = p_full + 2;          // [2] PV done -> softmax (O rescale)
   uint64_t *q_full = pv_done + 2;          // softmax (Q staged) -> MMA
-  uint64_t *o_full = q_full + 1;           // last PV of an item -> epilogue
-  uint64_t *o_free = o_full + 1;           // epilogue -> first PV of the next item
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_free + 1);
+  uint64_t *o_full = q_full + 1;           // [2] last PV of an item -> epilogue
+  uint64_t *o_free = o_full + 2;           // [2] epilogue done -> MMA / softmax
+  uint64_t *ml_full = o_free + 2;          // [2] softmax (m, l) published -> epilogue
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(ml_full + 2);
   float *xo = reinterpret_cast<float *>(smem + kOffX);
   float2 *xml = reinterpret_cast<float2 *>(smem + kOffML);
 
@@ -270,10 +292,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_init(s_full + i, 1);
       mbar_init(p_full + i, 128);
       mbar_init(pv_done + i, 1);
+      mbar_init(o_full + i, 1);
+      mbar_init(o_free + i, 128);
+      mbar_init(ml_full + i, 128);
     }
     mbar_init(q_full, 128);
-    mbar_init(o_full, 1);
-    mbar_init(o_free, 128);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -289,13 +312,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const int box_tok = p.page_size < kTile ? p.page_size : kTile;
       const uint32_t half_box_bytes = box_tok * 128;
       int stage = 0;
-      uint32_t phase = 0;
+      uint32_t phase = 0, n_prod = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         Item x;
         decode_item(p, it, x);
         for (int t = 0; t < x.nt; ++t) {
           const TileInfo ti = tile_info(p, x, t);
           mbar_wait(empty + stage, phase ^ 1);
+          trace_ev(p, 0, n_prod++);
           const int n_box = (ti.valid + box_tok - 1) / box_tok;
           mbar_arrive_expect_tx(full + stage, n_box * half_box_bytes * 4);
           uint8_t *st = smem + stage * kKVStageBytes;
@@ -314,78 +338,70 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ======================= MMA issuer (single thread) =======================
-    if (lane == 0) {
-      const uint32_t sKV = smem_u32(smem);
-      const uint32_t tO = tmem + kColO;
-      const uint32_t tQ = tmem + kColQ;
-      int stage = 0, prev_stage = 0;
-      uint32_t phase = 0;
-      uint32_t n = 0;  // global tile counter (S/P double buffer index = n & 1)
-      uint32_t item_idx = 0;
-      int rep = 1;
-      auto issue_pv = [&](uint32_t m, int st, bool first) {
-        mbar_wait(p_full + (m & 1), (m >> 1) & 1);
-        if (first) mbar_wait(o_free, (item_idx & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t tP = tmem + kColS + (m & 1) * 64;
-        const uint32_t vb = sKV + st * kKVStageBytes + 16384;
-        // copy c of the replicated rows owns tokens [c*64/rep, (c+1)*64/rep) of the tile:
-        // its k-steps run with every other copy's TMEM lanes masked off.
-        const int ksteps_per_copy = 4 / rep;
-#pragma unroll 1
-        for (int c = 0; c < rep; ++c) {
-          uint32_t mask[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) mask[q] = (rep == 1 || q / (4 / rep) == c) ? 0u : 0xffffffffu;
-#pragma unroll 1
-          for (int part = 0; part < 2; ++part) {
-#pragma unroll 1
-            for (int k = 0; k < ksteps_per_copy; ++k) {
-              const int kk = c * ksteps_per_copy + k;
-              const uint64_t b = umma_desc_sw128(vb + kk * 2048, 8192, 1024);
-              tc_mma_f16_ts(tO, tP + part * 32 + kk * 8, b, kIdescPV,
-                            (first && part == 0 && k == 0) ? 0u : 1u, mask);
-            }
-          }
-        }
-        tc_commit(empty + st);
-        tc_commit(pv_done + (m & 1));
-      };
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        Item x;
-        decode_item(p, it, x);
-        rep = rep_of(8 * x.w);
-        mbar_wait(q_full, item_idx & 1);
-        tc_fence_after();
-        for (int t = 0; t < x.nt; ++t) {
+    // ======================= MMA issuer (whole warp, one elected lane issues) =========
+    // Every lane runs the loop so all operands stay warp-uniform (uniform registers); the
+    // tcgen05.mma / commit instructions are issued by elect.sync's lane (CUTLASS pattern).
+    const uint32_t sKV = smem_u32(smem);
+    const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+    int stage = 0, prev_stage = 0;
+    uint32_t phase = 0;
+    uint32_t n = 0;  // global tile counter (S/P double buffer index = n & 1)
+    uint32_t item_idx = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++item_idx) {
+      Item x;
+      decode_item(p, it, x);
+      const int rep = __shfl_sync(0xffffffffu, x.rep, 0);
+      const uint32_t ob = item_idx & 1;  // O double buffer
+      const uint32_t tO = tmem_u + kColO + ob * 128;
+      mbar_wait(q_full, item_idx & 1);
+      if (lane == 0) trace_ev(p, 6, n);
+      tc_fence_after();
+      for (int t = 0; t <= x.nt; ++t) {
+        if (t < x.nt) {
           mbar_wait(full + stage, phase);
+          if (lane == 0) trace_ev(p, 1, n);
           tc_fence_after();
-          const uint32_t kb = sKV + stage * kKVStageBytes;
-          const uint32_t tS = tmem + kColS + (n & 1) * 64;
-          const uint32_t nomask[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t b = umma_desc_sw128(kb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
-            tc_mma_f16_ts(tS, tQ + kk * 8, b, kIdescQK, kk > 0 ? 1u : 0u, nomask);
+          if (elect_one()) {
+            issue_qk(tmem_u + kColS + (n & 1) * 64, tmem_u + kColQ, sKV + stage * kKVStageBytes);
+            tc_commit(s_full + (n & 1));
           }
-          tc_commit(s_full + (n & 1));
-          if (t > 0) issue_pv(n - 1, prev_stage, t == 1);
+          __syncwarp();
+          if (lane == 0) trace_ev(p, 2, n);
+        }
+        if (t > 0) {
+          // PV of the previous tile (its P is ready once the softmax arrives on p_full)
+          const uint32_t m = n - 1;
+          mbar_wait(p_full + (m & 1), (m >> 1) & 1);
+          if (lane == 0) trace_ev(p, 3, m);
+          const bool first = (t == 1);
+          // O[ob] is free once the epilogue of item item_idx - 2 has read it
+          if (first) mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t tP = tmem_u + kColS + (m & 1) * 64;
+            const uint32_t vb = sKV + prev_stage * kKVStageBytes + 16384;
+            if (rep == 4) issue_pv<4>(tO, tP, vb, first);
+            else if (rep == 2) issue_pv<2>(tO, tP, vb, first);
+            else issue_pv<1>(tO, tP, vb, first);
+            tc_commit(empty + prev_stage);
+            tc_commit(pv_done + (m & 1));
+            if (t == x.nt) tc_commit(o_full + ob);
+          }
+          __syncwarp();
+          if (lane == 0) trace_ev(p, 5, m);
+        }
+        if (t < x.nt) {
           prev_stage = stage;
           if (++stage == kStages) { stage = 0; phase ^= 1; }
           ++n;
         }
-        issue_pv(n - 1, prev_stage, x.nt == 1);
-        tc_commit(o_full);
-        ++item_idx;
       }
     }
-  } else {
-    // ======================= softmax / correction / epilogue (128 threads) ===========
+  } else if (warp < 6) {
+    // ======================= softmax / O correction (128 threads) =======================
     const int wq = warp & 3;            // TMEM lane quadrant of this warp
     const int mrow = wq * 32 + lane;    // M-row (TMEM lane) owned by this thread
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
-    const uint32_t tO = tmem + lane_off + kColO;
     uint32_t n = 0, item_idx = 0;
     if (blockIdx.x < n_items) {
       Item x0;
@@ -395,21 +411,24 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tc_fence_before();
       mbar_arrive(q_full);
     }
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++item_idx) {
       Item x;
       decode_item(p, it, x);
       const int R8 = 8 * x.w;
-      const int rep = rep_of(R8);
+      const int rep = x.rep;
       const int rpc = 128 / rep, cw = 64 / rep;
       const int copy = mrow / rpc, i = mrow - copy * rpc;
       const int colbase = copy * cw;
+      const uint32_t ob = item_idx & 1;
+      const uint32_t tO = tmem + lane_off + kColO + ob * 128;
       float m_run = -INFINITY, l_run = 0.f;
       for (int t = 0; t < x.nt; ++t) {
         const uint32_t sb = n & 1;
-        const TileInfo ti = tile_info(p, x, t);
-        const bool live = i < R8 && (ti.jrow < 0 || (i >> 3) == ti.jrow);
-        const int nvalid = max(0, min(cw, ti.valid - colbase));
+        const int2 tr = tile_rows(p, x, t);  // {valid tokens, owning branch or -1}
+        const bool live = i < R8 && (tr.y < 0 || (i >> 3) == tr.y);
+        const int nvalid = max(0, min(cw, tr.x - colbase));
         mbar_wait(s_full + sb, (n >> 1) & 1);
+        if (warp == 2 && lane == 0) trace_ev(p, 7, n);
         tc_fence_after();
         // P[sb] aliases S[sb]: PV(n-2) finished reading it before QK(n) was issued.
         const uint32_t tS = tmem + lane_off + kColS + sb * 64;
@@ -426,6 +445,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           softmax_tile<64>(tS, colbase, nvalid, live, o_live, p.scale_log2, m_run, l_run, tO,
                            pv_prev, pv_par);
         tc_fence_before();
+        if (warp == 2 && lane == 0) trace_ev(p, 8, n);
         mbar_arrive(p_full + sb);
         ++n;
       }
@@ -439,38 +459,62 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tc_fence_before();
         mbar_arrive(q_full);
       }
-      // ---- epilogue: merge the copies of each stacked row, write the partial (o, lse)
-      mbar_wait(o_full, item_idx & 1);
+      // publish (m, l) for the epilogue warps; xml[ob] was consumed by epilogue item_idx-2
+      mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);
+      xml[ob * 128 + mrow] = make_float2(m_run, l_run);
+      mbar_arrive(ml_full + ob);
+    }
+  } else {
+    // ======================= epilogue (128 threads, warps 6-9) =======================
+    // Merges the replicated copies of each stacked row and writes the normalised partial
+    // (o, lse), overlapping the next item's tiles (O is double-buffered in TMEM).
+    const int wq = warp & 3;
+    const int mrow = wq * 32 + lane;
+    const uint32_t lane_off = uint32_t(wq * 32) << 16;
+    uint32_t item_idx = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++item_idx) {
+      Item x;
+      decode_item(p, it, x);
+      const int R8 = 8 * x.w;
+      const int rep = x.rep;
+      const int rpc = 128 / rep;
+      const int copy = mrow / rpc, i = mrow - copy * rpc;
+      const uint32_t ob = item_idx & 1;
+      const uint32_t tO = tmem + lane_off + kColO + ob * 128;
+      mbar_wait(ml_full + ob, (item_idx >> 1) & 1);
+      mbar_wait(o_full + ob, (item_idx >> 1) & 1);
+      if (warp == 6 && lane == 0) trace_ev(p, 10, item_idx);
       tc_fence_after();
-      xml[mrow] = make_float2(m_run, l_run);
-      named_bar_sync(1, 128);
+      const float2 mine = xml[ob * 128 + mrow];
       float M = -INFINITY, L = 0.f;
-      for (int c = 0; c < rep; ++c) M = fmaxf(M, xml[c * rpc + i].x);
+      for (int c = 0; c < rep; ++c) M = fmaxf(M, xml[ob * 128 + c * rpc + i].x);
       for (int c = 0; c < rep; ++c) {
-        const float2 ml = xml[c * rpc + i];
+        const float2 ml = xml[ob * 128 + c * rpc + i];
         if (ml.y > 0.f) L += ex2(ml.x - M) * ml.y;
       }
-      const float f = (L > 0.f && l_run > 0.f) ? ex2(m_run - M) / L : 0.f;
+      const float f = (L > 0.f && mine.y > 0.f) ? ex2(mine.x - M) / L : 0.f;
       const bool out_row = i < R8;
       const bool warp_out = __any_sync(0xffffffffu, out_row);
       // copies 1..rep-1 park their scaled rows in SMEM; copy 0 adds them and stores
-      if (warp_out && copy > 0) {
+      if (rep > 1) {
+        if (warp_out && copy > 0) {
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tmem_ld32(tO + c * 32, o);
-          tmem_ld_wait();
-          if (out_row) {
-            float4 *xr = reinterpret_cast<float4 *>(xo + ((copy - 1) * rpc + i) * kHeadDim) + c * 8;
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait();
+            if (out_row) {
+              float4 *xr = reinterpret_cast<float4 *>(xo + ((copy - 1) * rpc + i) * kXStride) + c * 8;
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              xr[j] = make_float4(__uint_as_float(o[4 * j]) * f, __uint_as_float(o[4 * j + 1]) * f,
-                                  __uint_as_float(o[4 * j + 2]) * f,
-                                  __uint_as_float(o[4 * j + 3]) * f);
+              for (int j = 0; j < 8; ++j)
+                xr[j] = make_float4(__uint_as_float(o[4 * j]) * f, __uint_as_float(o[4 * j + 1]) * f,
+                                    __uint_as_float(o[4 * j + 2]) * f,
+                                    __uint_as_float(o[4 * j + 3]) * f);
+            }
           }
         }
+        named_bar_sync(2, 128);
       }
-      named_bar_sync(1, 128);
       if (warp_out && copy == 0) {
         const size_t prow = ((size_t)(x.cs0 + (i >> 3)) * h + x.g) * kGroup + (i & 7);
         if (out_row)
@@ -489,7 +533,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                                      __uint_as_float(o[4 * j + 3]) * f);
               for (int cc = 1; cc < rep; ++cc) {
                 const float4 b = reinterpret_cast<const float4 *>(
-                    xo + ((cc - 1) * rpc + i) * kHeadDim)[c * 8 + j];
+                    xo + ((cc - 1) * rpc + i) * kXStride)[c * 8 + j];
                 a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
               }
               d4[c * 8 + j] = a;
@@ -497,9 +541,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           }
         }
       }
+      if (rep > 1) named_bar_sync(2, 128);  // X reused by the next epilogue
       tc_fence_before();
-      mbar_arrive(o_free);
-      ++item_idx;
+      if (warp == 6 && lane == 0) trace_ev(p, 11, item_idx);
+      mbar_arrive(o_free + ob);
     }
   }
   tc_fence_before();
@@ -618,6 +663,14 @@ static int make_kv_map(CUtensorMap *map, const void *pool, const taper_kv *kv) {
 }
 
 static thread_local cudaEvent_t g_prof_ev[3] = {nullptr, nullptr, nullptr};
+static thread_local long long *g_trace = nullptr;
+static thread_local int g_trace_cap = 0;
+
+extern "C" int taper_set_trace_buffer(void *device_buffer, int capacity_tiles) {
+  g_trace = static_cast<long long *>(device_buffer);
+  g_trace_cap = device_buffer ? capacity_tiles : 0;
+  return TAPER_OK;
+}
 
 extern "C" int taper_set_profile_events(void *const *events, int n_events) {
   if (events && n_events != 3) return fail(TAPER_ERR_ARG, "need 3 events");
@@ -660,8 +713,6 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   if (S == 0) { set_launches(0); return TAPER_OK; }
   const int h = kv->h_local;
   char *w = static_cast<char *>(workspace);
-  size_t lse_off, o_off;
-  ws_partials(workspace_bytes, R, S, h, &lse_off, &o_off);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
   CUtensorMap tmK, tmV;
@@ -677,26 +728,24 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
     if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(attend_kernel)");
     attr_set = true;
   }
+  WsTables tabs = ws_tables(workspace_bytes, R, S, h);
   AttnParams ap;
-  ap.Lsh = batch->req_shared_len;
-  ap.Lloc = batch->slot_local_len;
-  ap.req_page_off = kv->req_page_off;
-  ap.req_pages = kv->req_pages;
   ap.slot_page_off = kv->slot_page_off;
   ap.slot_pages = kv->slot_pages;
+  ap.req_page_off = kv->req_page_off;
+  ap.req_pages = kv->req_pages;
   ap.hdr = reinterpret_cast<const int32_t *>(w + L.hdr);
-  ap.req_chunk_off = reinterpret_cast<const int32_t *>(w + L.req_chunk_off);
-  ap.req_loc_off = reinterpret_cast<const int32_t *>(w + L.req_loc_off);
-  ap.req_part_off = reinterpret_cast<const int32_t *>(w + L.req_part_off);
-  ap.req_adm_off = reinterpret_cast<const int32_t *>(w + L.req_adm_off);
   ap.adm_by_req = reinterpret_cast<const int32_t *>(w + L.adm_by_req);
+  ap.items = reinterpret_cast<const ItemDesc *>(w + tabs.items);
+  ap.ltiles = reinterpret_cast<const int4 *>(w + tabs.ltiles);
   ap.q = static_cast<const __nv_bfloat16 *>(q);
-  ap.part_lse = reinterpret_cast<float *>(w + lse_off);
-  ap.part_o = reinterpret_cast<float *>(w + o_off);
-  ap.R = R;
+  ap.part_lse = reinterpret_cast<float *>(w + tabs.lse);
+  ap.part_o = reinterpret_cast<float *>(w + tabs.o);
   ap.h_local = h;
   ap.page_size = kv->page_size;
   ap.scale_log2 = scale * 1.4426950408889634f;
+  ap.trace = g_trace;
+  ap.trace_cap = g_trace_cap;
   const int sms = device_sms();
   if (g_prof_ev[0]) cudaEventRecord(g_prof_ev[0], st);
   attend_kernel<<<sms, kAttnThreads, kSmemBytes, st>>>(tmK, tmV, ap);
@@ -708,10 +757,10 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   mp.hdr = ap.hdr;
   mp.slot_req = reinterpret_cast<const int32_t *>(w + L.slot_req);
   mp.slot_rank = reinterpret_cast<const int32_t *>(w + L.slot_rank);
-  mp.req_chunk_off = ap.req_chunk_off;
-  mp.req_loc_off = ap.req_loc_off;
-  mp.req_part_off = ap.req_part_off;
-  mp.req_adm_off = ap.req_adm_off;
+  mp.req_chunk_off = reinterpret_cast<const int32_t *>(w + L.req_chunk_off);
+  mp.req_loc_off = reinterpret_cast<const int32_t *>(w + L.req_loc_off);
+  mp.req_part_off = reinterpret_cast<const int32_t *>(w + L.req_part_off);
+  mp.req_adm_off = reinterpret_cast<const int32_t *>(w + L.req_adm_off);
   mp.adm_list = adm->adm_list;
   mp.part_lse = ap.part_lse;
   mp.part_o = ap.part_o;

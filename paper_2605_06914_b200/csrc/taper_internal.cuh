@@ -48,24 +48,49 @@ __host__ __device__ inline WsLayout ws_layout(int R, int S) {
   return w;
 }
 
-// bytes of partial storage per chunk-slot (8 rows x 128 fp32 + 8 lse) per KV head;
-// a chunk-slot is one (work item, admitted slot) pair: prefix chunks and local items
+// Per chunk-slot (one (work item, admitted slot) pair: prefix chunks and local items) the
+// workspace holds, per KV head, 8 partial rows (128 fp32 o + 1 fp32 lse), plus one item
+// descriptor and 16 local-tile descriptors (items and local items never outnumber
+// chunk-slots because every item covers >= 1 admitted slot).
 constexpr size_t kPartBytesPerCsHead = size_t(kGroup) * (kHeadDim + 1) * sizeof(float);
+constexpr size_t kItemDescBytes = 32;                 // ItemDesc
+constexpr size_t kLocalTileBytes = 16;                // int4 {slot, tok0, valid, jrow}
+constexpr size_t kWorkBytesPerCs = kItemDescBytes + kLocalItemTiles * kLocalTileBytes;
+
+// Work item descriptor emitted by the admission kernel (A5).  Items are numbered per KV
+// head: prefix chunks of all requests first (request-major), then local items.
+struct ItemDesc {
+  int32_t r;        // request
+  int32_t w;        // admitted branches (stacked rows = 8 w)
+  int32_t adm_off;  // first admitted slot of r in adm_by_req
+  int32_t cs0;      // chunk-slot of this item's first stacked branch
+  int32_t tb;       // prefix chunk: first token; local item: first local-tile entry
+  int32_t te;       // prefix chunk: end token;   local item: unused
+  int32_t nt;       // 64-token tiles
+  int32_t flags;    // bit 0: local item; bits 1..: replication factor (1, 2, 4)
+};
 
 __host__ __device__ inline int64_t ws_cap_cs(size_t bytes, int R, int S, int h_local) {
   WsLayout w = ws_layout(R, S);
-  if (bytes < w.fixed + 512) return 0;
-  return int64_t((bytes - w.fixed - 512) / (kPartBytesPerCsHead * size_t(h_local)));
+  if (bytes < w.fixed + 1024) return 0;
+  return int64_t((bytes - w.fixed - 1024) / (kPartBytesPerCsHead * size_t(h_local) + kWorkBytesPerCs));
 }
 
-// part_lse then part_o, each indexed by partial row
-//   prow = ((cs * h_local + g) * 8 + qh)
-__host__ __device__ inline void ws_partials(size_t bytes, int R, int S, int h_local,
-                                            size_t *lse_off, size_t *o_off) {
+// part_lse, part_o (partial row prow = ((cs * h_local + g) * 8 + qh)), item descriptors,
+// local-tile descriptors
+struct WsTables {
+  size_t lse, o, items, ltiles;
+  int64_t cap_cs;
+};
+__host__ __device__ inline WsTables ws_tables(size_t bytes, int R, int S, int h_local) {
   WsLayout w = ws_layout(R, S);
-  int64_t cap = ws_cap_cs(bytes, R, S, h_local);
-  *lse_off = w.fixed;
-  *o_off = ws_align(w.fixed + size_t(cap) * h_local * kGroup * sizeof(float));
+  WsTables t;
+  t.cap_cs = ws_cap_cs(bytes, R, S, h_local);
+  t.lse = w.fixed;
+  t.o = ws_align(t.lse + size_t(t.cap_cs) * h_local * kGroup * sizeof(float));
+  t.items = ws_align(t.o + size_t(t.cap_cs) * h_local * kGroup * kHeadDim * sizeof(float));
+  t.ltiles = ws_align(t.items + size_t(t.cap_cs) * kItemDescBytes);
+  return t;
 }
 
 // ------------------------------------------------------------------ PTX wrappers

@@ -25,7 +25,7 @@ TAPER_MAX_SLOTS = 4096
 TAPER_CHUNK_TOKENS = 1024
 EXPORTS = ("taper_workspace_size", "taper_admit", "taper_build_work", "taper_decode_attention",
            "taper_status_string", "taper_last_error", "taper_last_launch_count",
-           "taper_set_profile_events")
+           "taper_set_profile_events", "taper_set_trace_buffer")
 
 _vp = ctypes.c_void_p
 
@@ -75,6 +75,8 @@ def load_library() -> ctypes.CDLL:
     lib.taper_status_string.argtypes = [ctypes.c_int]
     lib.taper_last_error.restype = ctypes.c_char_p
     lib.taper_last_launch_count.restype = ctypes.c_int
+    lib.taper_set_trace_buffer.restype = ctypes.c_int
+    lib.taper_set_trace_buffer.argtypes = [_vp, ctypes.c_int]
     lib.taper_set_profile_events.restype = ctypes.c_int
     lib.taper_set_profile_events.argtypes = [_vp, ctypes.c_int]
     for name in ("taper_workspace_size", "taper_admit", "taper_build_work",
@@ -121,6 +123,12 @@ def taper_set_profile_events(events) -> None:
         return
     arr = (_vp * 3)(*[e.cuda_event for e in events])
     _check(_lib.taper_set_profile_events(arr, 3), "taper_set_profile_events")
+
+
+def taper_set_trace_buffer(buf, capacity_tiles: int = 0) -> None:
+    """Debug: int64 device tensor [capacity_tiles * 16] receiving CTA 0's pipeline events."""
+    _check(_lib.taper_set_trace_buffer(None if buf is None else buf.data_ptr(),
+                                       capacity_tiles), "taper_set_trace_buffer")
 
 
 # ------------------------------------------------------------------ device-side containers

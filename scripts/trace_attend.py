@@ -1,0 +1,69 @@
+"""Dev tool: capture CTA 0's pipeline timeline of attend_kernel on one C2 layer and print
+per-tile intervals (clock64 cycles).  Usage (GPU box): python scripts/trace_attend.py [cfg]"""
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2605_06914_b200 import taper as T  # noqa: E402
+
+EV = ["tma_issue", "mma_full", "qk_commit", "pv_pfull", "pv_ofree", "pv_commit", "mma_qfull",
+      "sm_sfull", "sm_arrive", "ep_start", "ep_ofull", "ep_end"]
+
+
+def main():
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    b = synth.config_batch(cfg, seed=0)
+    lay = synth.make_layout(b, 64, np.random.default_rng(1), 1)
+    db = T.DeviceBatch.from_host(b)
+    adm = T.DeviceAdmission.empty(b.n_req, b.n_slot)
+    ws = torch.empty(T.taper_workspace_size(b.n_req, b.n_slot, 8, T.max_chunk_slots(
+        b.req_shared_len, b.req_slot_off, b.slot_local_len)), dtype=torch.uint8, device="cuda")
+    T.taper_admit(db, (12.0, 0.03, 2e-5), "eager", 0.8, adm, 8, ws)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    shape = (lay.num_pages, 8, 64, 128)
+    k = torch.randn(shape, generator=g, device="cuda", dtype=torch.bfloat16)
+    v = torch.randn(shape, generator=g, device="cuda", dtype=torch.bfloat16)
+    rpo, rp, spo, sp = T.page_tables_to_device(lay)
+    kv = T.DeviceKV(k, v, rpo, rp, spo, sp)
+    q = torch.randn((b.n_slot, 64, 128), generator=g, device="cuda", dtype=torch.bfloat16)
+    out = torch.empty_like(q)
+    for _ in range(3):
+        T.taper_decode_attention(db, adm, kv, q, out, None, 1 / math.sqrt(128), ws)
+    cap = 4096
+    tr = torch.zeros(cap * 16, dtype=torch.int64, device="cuda")
+    T.taper_set_trace_buffer(tr, cap)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    T.taper_decode_attention(db, adm, kv, q, out, None, 1 / math.sqrt(128), ws)
+    e1.record()
+    torch.cuda.synchronize()
+    T.taper_set_trace_buffer(None)
+    print(f"layer time {e0.elapsed_time(e1) * 1e3:.1f} us")
+    a = tr.view(cap, 16).cpu().numpy()
+    n = int((a[:, 1] > 0).sum())
+    a = a[:n].astype(np.int64)
+    t0 = a[0, 0]
+    a = np.where(a > 0, a - t0, -1)
+    np.save("gpurun_out/trace.npy", a)
+    print("tiles", n, "total cycles", a[n - 1, 5])
+    d = np.diff(a[:, 1])
+    print("mma_full interval: median", np.median(d), "mean", d.mean())
+    for name, (x, y) in {"tma->full": (0, 1), "full->qkcommit": (1, 2), "qk->sm_sfull": (2, 7),
+                         "sm_sfull->arrive": (7, 8), "arrive->pv_pfull": (8, 3),
+                         "pfull->pvcommit": (3, 5)}.items():
+        dd = a[:, y] - a[:, x]
+        ok = (a[:, x] >= 0) & (a[:, y] >= 0)
+        print(f"{name:18s} median {np.median(dd[ok]):8.0f} mean {dd[ok].mean():8.0f}")
+    print("first 40 tiles (cycles rel.):")
+    print("   n " + " ".join(f"{e[:9]:>9s}" for e in EV))
+    for i in range(min(40, n)):
+        print(f"{i:4d} " + " ".join(f"{x:9d}" for x in a[i, :12]))
+
+
+if __name__ == "__main__":
+    main()
