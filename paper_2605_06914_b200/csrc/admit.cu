@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     p.hdr[2] = n_adm;
     p.hdr[3] = int(p.cap_cs > 0x7fffffff ? 0x7fffffff : p.cap_cs);
     p.hdr[4] = p.h_local;
+    p.hdr[8] = 0;  // dynamic work counter of the next attend_kernel
     *p.n_adm = n_adm;
     if (p.decide) *p.status = st;
     else atomicOr(p.status, st);

@@ -37,17 +37,26 @@
 namespace taper {
 
 constexpr int kTile = kTileTokens;   // 64 tokens per pipeline stage
-constexpr int kStages = 5;           // TMA ring depth (5 x 32 KB in flight per SM)
-constexpr int kKVStageBytes = 4 * 8192;           // K[d0:64], K[d64:128], V[..], V[..]
-constexpr int kXStride = 132;                     // floats per exchange row (bank padding)
-constexpr int kOffX = kStages * kKVStageBytes;    // epilogue exchange: 96 rows
-constexpr int kXBytes = 96 * kXStride * 4;
+// K and V tiles ride separate TMA rings: a K stage is released as soon as QK(t) completes,
+// a V stage only after PV(t); each stage is 64 tokens x 128 d bf16 = two 8 KB boxes.
+constexpr int kKStages = 4;
+constexpr int kVStages = 6;
+constexpr int kStageBytes = 2 * 8192;
+constexpr int kOffV = kKStages * kStageBytes;                 // 64 KB
+constexpr int kOffQS = kOffV + kVStages * kStageBytes;        // 160 KB: next item's queries
+constexpr int kQSBytes = 128 * 256;                           // 128 rows x 128 bf16
+constexpr int kXCols = 32;                                    // epilogue pass width
+constexpr int kXStride = kXCols + 4;                          // floats per staged row (+pad)
+constexpr int kOffX = kOffQS + kQSBytes;                      // 192 KB: staging 128 rows
+constexpr int kXBytes = 128 * kXStride * 4;
 constexpr int kOffML = kOffX + kXBytes;           // (m, l) of the 128 M-rows, 2 buffers
 constexpr int kOffBar = kOffML + 2 * 128 * 8;
-constexpr int kSmemUsed = kOffBar + 256;
+constexpr int kItemRing = 8;                      // claimed-item broadcast ring
+constexpr int kSmemUsed = kOffBar + 512;
 constexpr int kSmemBytes = kSmemUsed + 1024;      // + alignment slack
-// warp 0: TMA producer; warp 1: MMA issuer; warps 2-5: softmax; warps 6-9: epilogue
-constexpr int kAttnThreads = 320;
+// warp 0: item claimer + K producer; warp 1: MMA issuer; warps 2-5: softmax;
+// warps 6-9: epilogue; warp 10: V producer
+constexpr int kAttnThreads = 352;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0;     // S0 / P0 [0, 64), S1 / P1 [64, 128)
 constexpr uint32_t kColO = 128;   // O0 [128, 256), O1 [256, 384)
@@ -64,6 +73,7 @@ struct AttnParams {
   const __nv_bfloat16 *q;
   float *part_lse, *part_o;
   int h_local, page_size;
+  int tma5d;  // 1: page_size >= 64, one 5-D box per tile; 0: two 4-D boxes per page
   float scale_log2;
   long long *trace;  // debug: pipeline event timestamps of CTA 0 (taper_set_trace_buffer)
   int trace_cap;
@@ -119,27 +129,40 @@ __device__ __forceinline__ int2 tile_rows(const AttnParams &p, const Item &x, in
   return make_int2(lt.z, lt.w);
 }
 
-// Stage the (replicated) stacked queries of an item into TMEM columns [kColQ, kColQ+64).
-__device__ __forceinline__ void load_q_tmem(const AttnParams &p, const Item &x, uint32_t tmem,
-                                            uint32_t lane_off, int mrow) {
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Move the item's staged stacked queries (SMEM, [row][128] bf16, filled by the producer's
+// bulk copies) into TMEM columns [kColQ, kColQ+64), replicated over the row copies; then
+// release the staging buffer.  Ends with the tcgen05 stores complete and fenced.
+__device__ __forceinline__ void stage_q_tmem(const Item &x, const uint8_t *qs, uint64_t *qs_full,
+                                             uint64_t *qs_free, uint32_t item_k, uint32_t tmem,
+                                             uint32_t lane_off, int mrow) {
   const int R8 = 8 * x.w;
   const int rpc = 128 / x.rep;
   const int i = mrow % rpc;
+  mbar_wait(qs_full, item_k & 1);
   uint32_t v[64];
   if (i < R8) {
-    const int slot = __ldg(p.adm_by_req + x.adm_off + (i >> 3));
-    const uint4 *src = reinterpret_cast<const uint4 *>(
-        p.q + ((size_t)slot * (kGroup * p.h_local) + x.g * kGroup + (i & 7)) * kHeadDim);
+    const uint4 *src = reinterpret_cast<const uint4 *>(qs + i * 256);
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
-      const uint4 u = __ldg(src + c);
+      const uint4 u = src[c];
       v[4 * c] = u.x; v[4 * c + 1] = u.y; v[4 * c + 2] = u.z; v[4 * c + 3] = u.w;
     }
   } else {
 #pragma unroll
     for (int c = 0; c < 64; ++c) v[c] = 0u;
   }
+  mbar_arrive(qs_free);
   tmem_st_n<64>(tmem + lane_off + kColQ, v);
+  tmem_st_wait();
+  tc_fence_before();
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -188,30 +211,25 @@ __device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t vb, 
   }
 }
 
-// One tile of the online softmax for a thread's row.  CW = tokens of the tile owned by
-// this row's copy.  Updates m_run / l_run and writes P (hi, lo) into the row's S columns.
+// One tile of the online softmax for a thread's row, branch-free.  CW = tokens of the tile
+// owned by this row's copy; nvalid = live tokens among them (0 for a row that is dead in
+// this tile).  Updates m_run / l_run and writes P (hi, lo) into the row's S columns.
 template <int CW>
-__device__ __forceinline__ void softmax_tile(uint32_t tS, int colbase, int nvalid, bool live,
-                                             bool o_live, float scale_log2, float &m_run,
-                                             float &l_run, uint32_t tO, uint64_t *pv_prev,
-                                             uint32_t pv_prev_parity) {
+__device__ __forceinline__ void softmax_tile(uint32_t tS, int colbase, int nvalid, bool o_live,
+                                             float c, float &m_run, float &l_run, uint32_t tO,
+                                             uint64_t *pv_prev, uint32_t pv_prev_parity) {
   uint32_t s[CW];
   tmem_ld_n<CW>(tS + colbase, s);
   tmem_ld_wait();
-  float mx = -INFINITY;
-  if (live) {
-    if (nvalid == CW) {
+  float x[CW];
 #pragma unroll
-      for (int j = 0; j < CW; ++j) mx = fmaxf(mx, __uint_as_float(s[j]));
-    } else {
+  for (int j = 0; j < CW; ++j) x[j] = j < nvalid ? __uint_as_float(s[j]) : -INFINITY;
+  float mx = x[0];
 #pragma unroll
-      for (int j = 0; j < CW; ++j)
-        if (j < nvalid) mx = fmaxf(mx, __uint_as_float(s[j]));
-    }
-    mx *= scale_log2;
-  }
+  for (int j = 1; j < CW; ++j) mx = fmaxf(mx, x[j]);
+  mx *= c;  // scores in log2 units (c = softmax scale * log2 e > 0)
   // lazy rescale: only raise the running max when it grows by more than 8 (log2 units)
-  const bool need = live && mx > m_run + 8.f;
+  const bool need = mx > m_run + 8.f;
   float alpha = 1.f;
   if (need) {
     alpha = ex2(m_run - mx);  // 0 when m_run = -inf
@@ -221,32 +239,29 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, int colbase, int nvali
   if (o_live && __any_sync(0xffffffffu, need)) {
     mbar_wait(pv_prev, pv_prev_parity);  // O *= alpha needs PV(n-1) complete
     tc_fence_after();
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
       uint32_t o[32];
-      tmem_ld32(tO + c * 32, o);
+      tmem_ld32(tO + q * 32, o);
       tmem_ld_wait();
 #pragma unroll
       for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-      tmem_st32(tO + c * 32, o);
+      tmem_st32(tO + q * 32, o);
     }
     tmem_st_wait();
   }
   // P = 2^(x - m) split into hi + lo bf16 (DESIGN.md Sec. 6 "P precision"), written back
   // into this row's S columns in groups of 16 tokens (8 packed columns per part)
+  const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
   float lsum = 0.f;
-  const float neg_m = -m_run;
 #pragma unroll
   for (int g16 = 0; g16 < CW / 16; ++g16) {
     uint32_t hi[8], lo[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
       const int j = g16 * 8 + jj;
-      float e0 = 0.f, e1 = 0.f;
-      if (live) {
-        if (2 * j < nvalid) e0 = ex2(fmaf(__uint_as_float(s[2 * j]), scale_log2, neg_m));
-        if (2 * j + 1 < nvalid) e1 = ex2(fmaf(__uint_as_float(s[2 * j + 1]), scale_log2, neg_m));
-      }
+      const float e0 = ex2(fmaf(x[2 * j], c, neg_m));
+      const float e1 = ex2(fmaf(x[2 * j + 1], c, neg_m));
       lsum += e0 + e1;
       const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
       const float2 f2 = __bfloat1622float2(h2);
@@ -261,6 +276,17 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, int colbase, int nvali
   tmem_st_wait();
 }
 
+// Consumer side of the claimed-item ring: the k-th item this CTA processes (-1 = done).
+__device__ __forceinline__ int ring_item(uint64_t *it_full, const int32_t *it_ring, uint32_t k) {
+  const uint32_t slot = k % kItemRing;
+  mbar_wait(it_full + slot, (k / kItemRing) & 1);
+  return *reinterpret_cast<const volatile int32_t *>(it_ring + slot);
+}
+__device__ __forceinline__ void ring_release(uint64_t *it_empty, uint32_t k, int lane) {
+  __syncwarp();
+  if (lane == 0) mbar_arrive(it_empty + (k % kItemRing));
+}
+
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attend_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   AttnParams p) {
@@ -269,16 +295,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   // keeps the shared address space (LDS/STS instead of generic loads)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kOffBar);
-  uint64_t *full = bars;                   // [kStages] TMA -> MMA
-  uint64_t *empty = bars + kStages;        // [kStages] MMA -> TMA
-  uint64_t *s_full = bars + 2 * kStages;   // [2] QK done -> softmax
+  uint64_t *kfull = bars;                      // [kKStages] TMA -> MMA (K tile landed)
+  uint64_t *kempty = kfull + kKStages;         // [kKStages] QK done -> TMA
+  uint64_t *vfull = kempty + kKStages;         // [kVStages] TMA -> MMA (V tile landed)
+  uint64_t *vempty = vfull + kVStages;         // [kVStages] PV done -> TMA
+  uint64_t *s_full = vempty + kVStages;        // [2] QK done -> softmax
   uint64_t *p_full = s_full + 2;           // [2] softmax -> PV
   uint64_t *pv_done = p_full + 2;          // [2] PV done -> softmax (O rescale)
   uint64_t *q_full = pv_done + 2;          // softmax (Q staged) -> MMA
   uint64_t *o_full = q_full + 1;           // [2] last PV of an item -> epilogue
   uint64_t *o_free = o_full + 2;           // [2] epilogue done -> MMA / softmax
   uint64_t *ml_full = o_free + 2;          // [2] softmax (m, l) published -> epilogue
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(ml_full + 2);
+  uint64_t *qs_full = ml_full + 2;         // producer's Q staging copy landed
+  uint64_t *qs_free = qs_full + 1;         // softmax moved the staged Q into TMEM
+  uint64_t *it_full = qs_free + 1;         // [kItemRing] producer claimed an item
+  uint64_t *it_empty = it_full + kItemRing;  // [kItemRing] 9 consumer warps read it
+  int32_t *it_ring = reinterpret_cast<int32_t *>(it_empty + kItemRing);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(it_ring + kItemRing);
   float *xo = reinterpret_cast<float *>(smem + kOffX);
   float2 *xml = reinterpret_cast<float2 *>(smem + kOffML);
 
@@ -286,8 +319,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const int h = p.h_local;
   const int n_items = (__ldg(p.hdr) + __ldg(p.hdr + 5)) * h;
 
+  // Zero the K/V rings once: rows of a partial tile that TMA does not load must hold finite
+  // values (P = 0 there, but 0 * NaN would still poison O).
+  for (int i = tid; i < kOffQS / 16; i += kAttnThreads)
+    reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
+  fence_proxy_async_smem();
   if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+    for (int i = 0; i < kKStages; ++i) { mbar_init(kfull + i, 1); mbar_init(kempty + i, 1); }
+    for (int i = 0; i < kVStages; ++i) { mbar_init(vfull + i, 1); mbar_init(vempty + i, 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + i, 1);
       mbar_init(p_full + i, 128);
@@ -297,6 +336,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_init(ml_full + i, 128);
     }
     mbar_init(q_full, 128);
+    mbar_init(qs_full, 1);
+    mbar_init(qs_free, 128);
+    for (int i = 0; i < kItemRing; ++i) { mbar_init(it_full + i, 1); mbar_init(it_empty + i, 10); }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -306,48 +348,116 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ======================= TMA producer =======================
-    if (lane == 0) {
-      const int box_tok = p.page_size < kTile ? p.page_size : kTile;
-      const uint32_t half_box_bytes = box_tok * 128;
-      int stage = 0;
-      uint32_t phase = 0, n_prod = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        Item x;
-        decode_item(p, it, x);
-        for (int t = 0; t < x.nt; ++t) {
-          const TileInfo ti = tile_info(p, x, t);
-          mbar_wait(empty + stage, phase ^ 1);
-          trace_ev(p, 0, n_prod++);
-          const int n_box = (ti.valid + box_tok - 1) / box_tok;
-          mbar_arrive_expect_tx(full + stage, n_box * half_box_bytes * 4);
-          uint8_t *st = smem + stage * kKVStageBytes;
-          for (int b = 0; b < n_box; ++b) {
-            const int tok = ti.tok0 + b * box_tok;
-            const int page = __ldg(ti.pages + tok / p.page_size);
-            const int row = tok % p.page_size;
-            const int o = b * half_box_bytes;
-            tma_load_4d(st + o, &tmK, full + stage, 0, row, x.g, page);
-            tma_load_4d(st + 8192 + o, &tmK, full + stage, 64, row, x.g, page);
-            tma_load_4d(st + 16384 + o, &tmV, full + stage, 0, row, x.g, page);
-            tma_load_4d(st + 24576 + o, &tmV, full + stage, 64, row, x.g, page);
-          }
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+  if (warp == 0 || warp == 10) {
+    // ======================= TMA producers: warp 0 = K (+ item claimer), warp 10 = V ====
+    // At each item start lane l resolves tile l's geometry and page indices (parallel
+    // loads); the tile loop then only shuffles them to the elected issuing lane, with
+    // warp-uniform operands (no per-instruction waterfall loops).
+    const bool is_k = warp == 0;
+    const CUtensorMap *tmap = is_k ? &tmK : &tmV;
+    uint64_t *ring_full = is_k ? kfull : vfull;
+    uint64_t *ring_empty = is_k ? kempty : vempty;
+    const int n_stages = is_k ? kKStages : kVStages;
+    uint8_t *ring = smem + (is_k ? 0 : kOffV);
+    const int box_tok = p.page_size < kTile ? p.page_size : kTile;
+    const uint32_t half_box_bytes = box_tok * 128;
+    uint32_t n_prod = 0;  // global tile counter
+    int *work_counter = const_cast<int *>(p.hdr) + 8;
+    for (uint32_t k = 0;; ++k) {
+      int it;
+      if (is_k) {
+        // claim the next item (dynamic scheduling) and broadcast it to the other roles
+        it = 0;
+        if (lane == 0) it = atomicAdd(work_counter, 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= n_items) it = -1;
+        const uint32_t slot = k % kItemRing;
+        mbar_wait(it_empty + slot, ((k / kItemRing) & 1) ^ 1);
+        if (lane == 0) {
+          *reinterpret_cast<volatile int32_t *>(it_ring + slot) = it;
+          mbar_arrive(it_full + slot);
         }
+        // the claimer also consumes its own slot
+        __syncwarp();
+        if (lane == 0) mbar_arrive(it_empty + slot);
+      } else {
+        it = ring_item(it_full, it_ring, k);
+        ring_release(it_empty, k, lane);
+      }
+      if (it < 0) break;
+      Item x;
+      decode_item(p, it, x);
+      if (is_k) {
+        // stage the item's stacked queries (w slots x 8 heads x 256 B, 2 KB per slot) in SMEM
+        // by bulk copies, so the softmax warps find them there at the item boundary
+        const int w_u = __shfl_sync(0xffffffffu, x.w, 0);
+        const int slot_j = lane < w_u ? __ldg(p.adm_by_req + x.adm_off + lane) : 0;
+        mbar_wait(qs_free, (k & 1) ^ 1);
+        if (elect_one()) mbar_arrive_expect_tx(qs_full, w_u * 2048);
+        __syncwarp();
+        for (int j = 0; j < w_u; ++j) {
+          const int s_j = __shfl_sync(0xffffffffu, slot_j, j);
+          const __nv_bfloat16 *src =
+              p.q + ((size_t)s_j * (kGroup * p.h_local) + x.g * kGroup) * kHeadDim;
+          if (elect_one()) bulk_g2s(smem + kOffQS + j * 2048, src, 2048, qs_full);
+          __syncwarp();
+        }
+      }
+      int my_tok0 = 0, my_valid = 0, my_pg[kTile / 16] = {0, 0, 0, 0};
+      if (lane < x.nt) {
+        const TileInfo ti = tile_info(p, x, lane);
+        my_tok0 = ti.tok0;
+        my_valid = ti.valid;
+#pragma unroll
+        for (int b = 0; b < kTile / 16; ++b)
+          if (b * box_tok < ti.valid) my_pg[b] = __ldg(ti.pages + (ti.tok0 + b * box_tok) / p.page_size);
+      }
+      const int g_u = __shfl_sync(0xffffffffu, x.g, 0);  // warp-uniform operands
+      const int nt_u = __shfl_sync(0xffffffffu, x.nt, 0);
+      for (int t = 0; t < nt_u; ++t, ++n_prod) {
+        const int tok0 = __shfl_sync(0xffffffffu, my_tok0, t);
+        const int valid = __shfl_sync(0xffffffffu, my_valid, t);
+        int pg[kTile / 16];
+#pragma unroll
+        for (int b = 0; b < kTile / 16; ++b) pg[b] = __shfl_sync(0xffffffffu, my_pg[b], t);
+        const uint32_t st = n_prod % n_stages;
+        const int n_box = (valid + box_tok - 1) / box_tok;
+        uint8_t *dst = ring + st * kStageBytes;
+        mbar_wait(ring_empty + st, ((n_prod / n_stages) & 1) ^ 1);
+        if (is_k && lane == 0) trace_ev(p, 0, n_prod);
+        if (elect_one()) {
+          if (p.tma5d) {
+            // one box: {64 d, 64 tokens, 2 d-halves} -> [d-half][token][64] (two SW128 atoms)
+            mbar_arrive_expect_tx(ring_full + st, 2 * kTile * 128);
+            tma_load_5d(dst, tmap, ring_full + st, 0, tok0 % p.page_size, 0, g_u, pg[0]);
+          } else {
+            mbar_arrive_expect_tx(ring_full + st, n_box * half_box_bytes * 2);
+#pragma unroll
+            for (int b = 0; b < kTile / 16; ++b) {
+              if (b < n_box) {
+                const int row = (tok0 + b * box_tok) % p.page_size;
+                const int o = b * half_box_bytes;
+                tma_load_4d(dst + o, tmap, ring_full + st, 0, row, g_u, pg[b]);
+                tma_load_4d(dst + 8192 + o, tmap, ring_full + st, 64, row, g_u, pg[b]);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (is_k && lane == 0) trace_ev(p, 12, n_prod);
       }
     }
   } else if (warp == 1) {
     // ======================= MMA issuer (whole warp, one elected lane issues) =========
     // Every lane runs the loop so all operands stay warp-uniform (uniform registers); the
     // tcgen05.mma / commit instructions are issued by elect.sync's lane (CUTLASS pattern).
-    const uint32_t sKV = smem_u32(smem);
+    const uint32_t sK = smem_u32(smem), sV = smem_u32(smem + kOffV);
     const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
-    int stage = 0, prev_stage = 0;
-    uint32_t phase = 0;
     uint32_t n = 0;  // global tile counter (S/P double buffer index = n & 1)
-    uint32_t item_idx = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++item_idx) {
+    for (uint32_t item_idx = 0;; ++item_idx) {
+      const int it = ring_item(it_full, it_ring, item_idx);
+      ring_release(it_empty, item_idx, lane);
+      if (it < 0) break;
       Item x;
       decode_item(p, it, x);
       const int rep = __shfl_sync(0xffffffffu, x.rep, 0);
@@ -358,11 +468,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tc_fence_after();
       for (int t = 0; t <= x.nt; ++t) {
         if (t < x.nt) {
-          mbar_wait(full + stage, phase);
+          const uint32_t ks = n % kKStages;
+          mbar_wait(kfull + ks, (n / kKStages) & 1);
           if (lane == 0) trace_ev(p, 1, n);
           tc_fence_after();
           if (elect_one()) {
-            issue_qk(tmem_u + kColS + (n & 1) * 64, tmem_u + kColQ, sKV + stage * kKVStageBytes);
+            issue_qk(tmem_u + kColS + (n & 1) * 64, tmem_u + kColQ, sK + ks * kStageBytes);
+            tc_commit(kempty + ks);
             tc_commit(s_full + (n & 1));
           }
           __syncwarp();
@@ -374,27 +486,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           mbar_wait(p_full + (m & 1), (m >> 1) & 1);
           if (lane == 0) trace_ev(p, 3, m);
           const bool first = (t == 1);
+          const uint32_t vs = m % kVStages;
           // O[ob] is free once the epilogue of item item_idx - 2 has read it
           if (first) mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);
+          mbar_wait(vfull + vs, (m / kVStages) & 1);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t tP = tmem_u + kColS + (m & 1) * 64;
-            const uint32_t vb = sKV + prev_stage * kKVStageBytes + 16384;
+            const uint32_t vb = sV + vs * kStageBytes;
             if (rep == 4) issue_pv<4>(tO, tP, vb, first);
             else if (rep == 2) issue_pv<2>(tO, tP, vb, first);
             else issue_pv<1>(tO, tP, vb, first);
-            tc_commit(empty + prev_stage);
+            tc_commit(vempty + vs);
             tc_commit(pv_done + (m & 1));
             if (t == x.nt) tc_commit(o_full + ob);
           }
           __syncwarp();
           if (lane == 0) trace_ev(p, 5, m);
         }
-        if (t < x.nt) {
-          prev_stage = stage;
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
-          ++n;
-        }
+        if (t < x.nt) ++n;
       }
     }
   } else if (warp < 6) {
@@ -402,16 +512,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int wq = warp & 3;            // TMEM lane quadrant of this warp
     const int mrow = wq * 32 + lane;    // M-row (TMEM lane) owned by this thread
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
-    uint32_t n = 0, item_idx = 0;
-    if (blockIdx.x < n_items) {
+    const float c_log2 = p.scale_log2;
+    uint32_t n = 0;
+    int it = ring_item(it_full, it_ring, 0);
+    if (it >= 0) {
       Item x0;
-      decode_item(p, blockIdx.x, x0);
-      load_q_tmem(p, x0, tmem, lane_off, mrow);
-      tmem_st_wait();
-      tc_fence_before();
+      decode_item(p, it, x0);
+      stage_q_tmem(x0, smem + kOffQS, qs_full, qs_free, 0, tmem, lane_off, mrow);
       mbar_arrive(q_full);
     }
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++item_idx) {
+    for (uint32_t item_idx = 0; it >= 0; ++item_idx) {
       Item x;
       decode_item(p, it, x);
       const int R8 = 8 * x.w;
@@ -426,7 +536,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const uint32_t sb = n & 1;
         const int2 tr = tile_rows(p, x, t);  // {valid tokens, owning branch or -1}
         const bool live = i < R8 && (tr.y < 0 || (i >> 3) == tr.y);
-        const int nvalid = max(0, min(cw, tr.x - colbase));
+        const int nvalid = live ? max(0, min(cw, tr.x - colbase)) : 0;
         mbar_wait(s_full + sb, (n >> 1) & 1);
         if (warp == 2 && lane == 0) trace_ev(p, 7, n);
         tc_fence_after();
@@ -436,33 +546,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const uint32_t pv_par = ((n - 1) >> 1) & 1;
         const bool o_live = t > 0;
         if (cw == 16)
-          softmax_tile<16>(tS, colbase, nvalid, live, o_live, p.scale_log2, m_run, l_run, tO,
-                           pv_prev, pv_par);
+          softmax_tile<16>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
         else if (cw == 32)
-          softmax_tile<32>(tS, colbase, nvalid, live, o_live, p.scale_log2, m_run, l_run, tO,
-                           pv_prev, pv_par);
+          softmax_tile<32>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
         else
-          softmax_tile<64>(tS, colbase, nvalid, live, o_live, p.scale_log2, m_run, l_run, tO,
-                           pv_prev, pv_par);
+          softmax_tile<64>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
         tc_fence_before();
-        if (warp == 2 && lane == 0) trace_ev(p, 8, n);
+        if (lane == 0) trace_ev(p, warp == 2 ? 8 : 6 + warp, n);  // warps 3,4,5 -> 9,10,11
         mbar_arrive(p_full + sb);
         ++n;
       }
       // all QK MMAs of this item are complete -> stage the next item's queries
-      const int next = it + gridDim.x;
-      if (next < n_items) {
+      const int next = ring_item(it_full, it_ring, item_idx + 1);
+      ring_release(it_empty, item_idx, lane);
+      if (next >= 0) {
         Item xn;
         decode_item(p, next, xn);
-        load_q_tmem(p, xn, tmem, lane_off, mrow);
-        tmem_st_wait();
-        tc_fence_before();
+        stage_q_tmem(xn, smem + kOffQS, qs_full, qs_free, item_idx + 1, tmem, lane_off, mrow);
         mbar_arrive(q_full);
       }
       // publish (m, l) for the epilogue warps; xml[ob] was consumed by epilogue item_idx-2
       mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);
       xml[ob * 128 + mrow] = make_float2(m_run, l_run);
       mbar_arrive(ml_full + ob);
+      it = next;
     }
   } else {
     // ======================= epilogue (128 threads, warps 6-9) =======================
@@ -471,8 +578,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int wq = warp & 3;
     const int mrow = wq * 32 + lane;
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
-    uint32_t item_idx = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++item_idx) {
+    for (uint32_t item_idx = 0;; ++item_idx) {
+      const int it = ring_item(it_full, it_ring, item_idx);
+      ring_release(it_empty, item_idx, lane);
+      if (it < 0) break;
       Item x;
       decode_item(p, it, x);
       const int R8 = 8 * x.w;
@@ -483,7 +592,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t tO = tmem + lane_off + kColO + ob * 128;
       mbar_wait(ml_full + ob, (item_idx >> 1) & 1);
       mbar_wait(o_full + ob, (item_idx >> 1) & 1);
-      if (warp == 6 && lane == 0) trace_ev(p, 10, item_idx);
+      if (warp == 6 && lane == 0) trace_ev(p, 10, 2048 + item_idx);
       tc_fence_after();
       const float2 mine = xml[ob * 128 + mrow];
       float M = -INFINITY, L = 0.f;
@@ -493,57 +602,49 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         if (ml.y > 0.f) L += ex2(ml.x - M) * ml.y;
       }
       const float f = (L > 0.f && mine.y > 0.f) ? ex2(mine.x - M) / L : 0.f;
+      if (warp == 6 && lane == 0) trace_ev(p, 12, 2048 + item_idx);
       const bool out_row = i < R8;
       const bool warp_out = __any_sync(0xffffffffu, out_row);
-      // copies 1..rep-1 park their scaled rows in SMEM; copy 0 adds them and stores
-      if (rep > 1) {
-        if (warp_out && copy > 0) {
+      const int etid = tid - 192;  // 0..127
+      if (out_row && copy == 0) {
+        const size_t prow = ((size_t)(x.cs0 + (i >> 3)) * h + x.g) * kGroup + (i & 7);
+        p.part_lse[prow] = L > 0.f ? (M + __log2f(L)) * 0.69314718055994531f : -INFINITY;
+      }
+      // four 32-column passes: every copy stages its scaled O row in SMEM, then all 128
+      // threads sum the copies and write the rows with coalesced stores
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tO + c * 32, o);
-            tmem_ld_wait();
-            if (out_row) {
-              float4 *xr = reinterpret_cast<float4 *>(xo + ((copy - 1) * rpc + i) * kXStride) + c * 8;
+      for (int half = 0; half < 4; ++half) {
+        if (warp_out) {
+          uint32_t o[32];
+          tmem_ld32(tO + half * 32, o);
+          tmem_ld_wait();
+          if (out_row) {
+            float4 *xr = reinterpret_cast<float4 *>(xo + mrow * kXStride);
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                xr[j] = make_float4(__uint_as_float(o[4 * j]) * f, __uint_as_float(o[4 * j + 1]) * f,
-                                    __uint_as_float(o[4 * j + 2]) * f,
-                                    __uint_as_float(o[4 * j + 3]) * f);
-            }
+            for (int j = 0; j < 8; ++j)
+              xr[j] = make_float4(__uint_as_float(o[4 * j]) * f, __uint_as_float(o[4 * j + 1]) * f,
+                                  __uint_as_float(o[4 * j + 2]) * f,
+                                  __uint_as_float(o[4 * j + 3]) * f);
           }
         }
         named_bar_sync(2, 128);
-      }
-      if (warp_out && copy == 0) {
-        const size_t prow = ((size_t)(x.cs0 + (i >> 3)) * h + x.g) * kGroup + (i & 7);
-        if (out_row)
-          p.part_lse[prow] = L > 0.f ? (M + __log2f(L)) * 0.69314718055994531f : -INFINITY;
-        float4 *d4 = reinterpret_cast<float4 *>(p.part_o + prow * kHeadDim);
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tmem_ld32(tO + c * 32, o);
-          tmem_ld_wait();
-          if (out_row) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float4 a = make_float4(__uint_as_float(o[4 * j]) * f, __uint_as_float(o[4 * j + 1]) * f,
-                                     __uint_as_float(o[4 * j + 2]) * f,
-                                     __uint_as_float(o[4 * j + 3]) * f);
-              for (int cc = 1; cc < rep; ++cc) {
-                const float4 b = reinterpret_cast<const float4 *>(
-                    xo + ((cc - 1) * rpc + i) * kXStride)[c * 8 + j];
-                a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-              }
-              d4[c * 8 + j] = a;
-            }
+        for (int k = etid; k < R8 * 8; k += 128) {
+          const int row = k >> 3, c4 = k & 7;
+          float4 a = reinterpret_cast<const float4 *>(xo + row * kXStride)[c4];
+          for (int cc = 1; cc < rep; ++cc) {
+            const float4 b = reinterpret_cast<const float4 *>(xo + (cc * rpc + row) * kXStride)[c4];
+            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
           }
+          const size_t prow = ((size_t)(x.cs0 + (row >> 3)) * h + x.g) * kGroup + (row & 7);
+          reinterpret_cast<float4 *>(p.part_o + prow * kHeadDim + half * kXCols)[c4] = a;
         }
+        if (warp == 8 && lane == 0 && half == 0) trace_ev(p, 13, 2048 + item_idx);
+        named_bar_sync(2, 128);  // staging reused by the next half / item
       }
-      if (rep > 1) named_bar_sync(2, 128);  // X reused by the next epilogue
+      if (warp == 6 && lane == 0) trace_ev(p, 14, 2048 + item_idx);
+      if (warp == 8 && lane == 0) trace_ev(p, 15, 2048 + item_idx);
       tc_fence_before();
-      if (warp == 6 && lane == 0) trace_ev(p, 11, item_idx);
+      if (warp == 6 && lane == 0) trace_ev(p, 11, 2048 + item_idx);
       mbar_arrive(o_free + ob);
     }
   }
@@ -569,6 +670,8 @@ struct MergeParams {
 
 __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
   const int lane = threadIdx.x & 31;
+  // the attend kernel of this call has finished (stream order): re-arm its work counter
+  if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<int32_t *>(p.hdr)[8] = 0;
   const int h = p.h_local;
   const int n_items = __ldg(p.hdr + 2) * h;
   const int qheads = kGroup * h;
@@ -649,15 +752,27 @@ static int make_kv_map(CUtensorMap *map, const void *pool, const taper_kv *kv) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return fail(TAPER_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t row = 128 * 2;
-  cuuint64_t dims[4] = {128, (cuuint64_t)kv->page_size, (cuuint64_t)kv->h_local,
-                        (cuuint64_t)kv->num_pages};
-  cuuint64_t strides[3] = {row, row * kv->page_size, row * kv->page_size * kv->h_local};
-  const cuuint32_t box_tok = kv->page_size < kTile ? kv->page_size : kTile;
-  cuuint32_t box[4] = {64, box_tok, 1, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(pool), dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const cuuint64_t ps = (cuuint64_t)kv->page_size, hl = (cuuint64_t)kv->h_local;
+  CUresult r;
+  if (kv->page_size >= kTile) {
+    // (d-lo 64, token, d-half 2, head, page): one {64, 64, 2} box = a full K or V tile in
+    // the [d-half][token][64] layout of two SW128 K-major atoms
+    cuuint64_t dims[5] = {64, ps, 2, hl, (cuuint64_t)kv->num_pages};
+    cuuint64_t strides[4] = {row, 128, row * ps, row * ps * hl};
+    cuuint32_t box[5] = {64, (cuuint32_t)kTile, 2, 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(pool), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[4] = {128, ps, hl, (cuuint64_t)kv->num_pages};
+    cuuint64_t strides[3] = {row, row * ps, row * ps * hl};
+    cuuint32_t box[4] = {64, (cuuint32_t)kv->page_size, 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(pool), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS) return fail(TAPER_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return TAPER_OK;
 }
@@ -743,6 +858,7 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   ap.part_o = reinterpret_cast<float *>(w + tabs.o);
   ap.h_local = h;
   ap.page_size = kv->page_size;
+  ap.tma5d = kv->page_size >= kTile ? 1 : 0;
   ap.scale_log2 = scale * 1.4426950408889634f;
   ap.trace = g_trace;
   ap.trace_cap = g_trace_cap;

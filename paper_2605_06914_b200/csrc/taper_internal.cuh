@@ -24,6 +24,7 @@ constexpr int kLocalItemTiles = 16;   // branch-local tiles per local work item
 // hdr[3] = cap_cs  : chunk-slot capacity of the partial buffers (for this h_local)
 // hdr[4] = h_local
 // hdr[5] = n_rl    : number of (request, local item) pairs (local items per KV head)
+// hdr[8] = work counter of attend_kernel's dynamic scheduler (reset by admit and merge)
 struct WsLayout {
   size_t hdr, slot_req, slot_rank, req_chunk_off, req_loc_off, req_part_off, req_adm_off,
       adm_by_req, part_lse, part_o, fixed;
@@ -143,6 +144,16 @@ __device__ __forceinline__ void tma_load_4d(void *smem_dst, const void *tmap, ui
       "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+// TMA: 5-D tiled load (one box lands both 64-column halves of a K or V tile).
+__device__ __forceinline__ void tma_load_5d(void *smem_dst, const void *tmap, uint64_t *bar,
+                                            int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
       "r"(smem_u32(bar))
       : "memory");
 }

@@ -59,6 +59,21 @@ def main():
         dd = a[:, y] - a[:, x]
         ok = (a[:, x] >= 0) & (a[:, y] >= 0)
         print(f"{name:18s} median {np.median(dd[ok]):8.0f} mean {dd[ok].mean():8.0f}")
+    full = tr.view(cap, 16).cpu().numpy().astype(np.int64)
+    ep = np.where(full[2048:2048 + 40] > 0, full[2048:2048 + 40] - t0, -1)
+    print("epilogue per item: ofull->ml, ml->xdone, xdone->bar, bar->stores(w8), stores->end")
+    for i in range(12):
+        r = ep[i]
+        print(i, r[12] - r[10], r[13] - r[12], r[14] - r[13], r[15] - r[14], r[11] - r[15])
+    arr = a[:, [8, 9, 10, 11]]
+    ok = (arr > 0).all(1)
+    lag = arr[ok] - arr[ok].min(1, keepdims=True)
+    print("softmax arrive lag per warp (2,3,4,5): median", np.median(lag, 0), "mean", lag.mean(0))
+    print("slowest warp histogram", np.bincount(arr[ok].argmax(1), minlength=4))
+    print("producer: top(15) kempty-ok(0) K-issued(12) vempty-ok(13) V-issued(14)")
+    for i in range(1, 12):
+        r = a[i]
+        print(i, r[15], r[0] - r[15], r[12] - r[0], r[13] - r[12], r[14] - r[13], "next top", a[i + 1][15] - r[14])
     print("first 40 tiles (cycles rel.):")
     print("   n " + " ".join(f"{e[:9]:>9s}" for e in EV))
     for i in range(min(40, n)):
