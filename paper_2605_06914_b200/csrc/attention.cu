@@ -39,15 +39,16 @@ namespace taper {
 constexpr int kTile = kTileTokens;   // 64 tokens per pipeline stage
 // K and V tiles ride separate TMA rings: a K stage is released as soon as QK(t) completes,
 // a V stage only after PV(t); each stage is 64 tokens x 128 d bf16 = two 8 KB boxes.
-constexpr int kKStages = 4;
-constexpr int kVStages = 6;
+constexpr int kKStages = 6;
+constexpr int kVStages = 5;
 constexpr int kStageBytes = 2 * 8192;
 constexpr int kOffV = kKStages * kStageBytes;                 // 64 KB
 constexpr int kOffQS = kOffV + kVStages * kStageBytes;        // 160 KB: next item's queries
-constexpr int kQSBytes = 128 * 256;                           // 128 rows x 128 bf16
-constexpr int kXCols = 32;                                    // epilogue pass width
+constexpr int kQSRows = 64;                                   // staged rows per pass
+constexpr int kQSBytes = kQSRows * 256;                       // 64 rows x 128 bf16
+constexpr int kXCols = 16;                                    // epilogue pass width
 constexpr int kXStride = kXCols + 4;                          // floats per staged row (+pad)
-constexpr int kOffX = kOffQS + kQSBytes;                      // 192 KB: staging 128 rows
+constexpr int kOffX = kOffQS + kQSBytes;                      // epilogue staging 128 rows
 constexpr int kXBytes = 128 * kXStride * 4;
 constexpr int kOffML = kOffX + kXBytes;           // (m, l) of the 128 M-rows, 2 buffers
 constexpr int kOffBar = kOffML + 2 * 128 * 8;
@@ -138,28 +139,30 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 
 // Move the item's staged stacked queries (SMEM, [row][128] bf16, filled by the producer's
-// bulk copies) into TMEM columns [kColQ, kColQ+64), replicated over the row copies; then
-// release the staging buffer.  Ends with the tcgen05 stores complete and fenced.
+// bulk copies in passes of 64 rows) into TMEM columns [kColQ, kColQ+64), replicated over
+// the row copies; each pass's buffer is released after use.  Ends with the tcgen05 stores
+// complete and fenced.  `pass` counts staging passes consumed so far (updated).
 __device__ __forceinline__ void stage_q_tmem(const Item &x, const uint8_t *qs, uint64_t *qs_full,
-                                             uint64_t *qs_free, uint32_t item_k, uint32_t tmem,
+                                             uint64_t *qs_free, uint32_t &pass, uint32_t tmem,
                                              uint32_t lane_off, int mrow) {
   const int R8 = 8 * x.w;
   const int rpc = 128 / x.rep;
   const int i = mrow % rpc;
-  mbar_wait(qs_full, item_k & 1);
   uint32_t v[64];
-  if (i < R8) {
-    const uint4 *src = reinterpret_cast<const uint4 *>(qs + i * 256);
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const uint4 u = src[c];
-      v[4 * c] = u.x; v[4 * c + 1] = u.y; v[4 * c + 2] = u.z; v[4 * c + 3] = u.w;
+  for (int c = 0; c < 64; ++c) v[c] = 0u;
+  for (int r0 = 0; r0 < R8; r0 += kQSRows, ++pass) {
+    mbar_wait(qs_full, pass & 1);
+    if (i >= r0 && i < min(R8, r0 + kQSRows)) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(qs + (i - r0) * 256);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const uint4 u = src[c];
+        v[4 * c] = u.x; v[4 * c + 1] = u.y; v[4 * c + 2] = u.z; v[4 * c + 3] = u.w;
+      }
     }
-  } else {
-#pragma unroll
-    for (int c = 0; c < 64; ++c) v[c] = 0u;
+    mbar_arrive(qs_free);
   }
-  mbar_arrive(qs_free);
   tmem_st_n<64>(tmem + lane_off + kColQ, v);
   tmem_st_wait();
   tc_fence_before();
@@ -198,8 +201,9 @@ __device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t vb, 
     uint32_t mask[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) mask[q] = (REP == 1 || q / (4 / REP) == c) ? 0u : 0xffffffffu;
+    constexpr int kParts = 2;  // P = hi + lo
 #pragma unroll
-    for (int part = 0; part < 2; ++part) {
+    for (int part = 0; part < kParts; ++part) {
 #pragma unroll
       for (int k = 0; k < KPC; ++k) {
         const int kk = c * KPC + k;
@@ -318,6 +322,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int h = p.h_local;
   const int n_items = (__ldg(p.hdr) + __ldg(p.hdr + 5)) * h;
+  if (p.trace != nullptr && tid == 0) {  // per-CTA wall-clock span (debug trace)
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    p.trace[(size_t)(3000 + blockIdx.x) * 16 + 0] = (long long)g;
+  }
 
   // Zero the K/V rings once: rows of a partial tile that TMA does not load must hold finite
   // values (P = 0 there, but 0 * NaN would still poison O).
@@ -362,6 +371,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int box_tok = p.page_size < kTile ? p.page_size : kTile;
     const uint32_t half_box_bytes = box_tok * 128;
     uint32_t n_prod = 0;  // global tile counter
+    uint32_t qs_pass = 0;  // query staging passes issued
     int *work_counter = const_cast<int *>(p.hdr) + 8;
     for (uint32_t k = 0;; ++k) {
       int it;
@@ -389,18 +399,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       decode_item(p, it, x);
       if (is_k) {
         // stage the item's stacked queries (w slots x 8 heads x 256 B, 2 KB per slot) in SMEM
-        // by bulk copies, so the softmax warps find them there at the item boundary
+        // by bulk copies (passes of 8 slots), so the softmax warps find them there
         const int w_u = __shfl_sync(0xffffffffu, x.w, 0);
         const int slot_j = lane < w_u ? __ldg(p.adm_by_req + x.adm_off + lane) : 0;
-        mbar_wait(qs_free, (k & 1) ^ 1);
-        if (elect_one()) mbar_arrive_expect_tx(qs_full, w_u * 2048);
-        __syncwarp();
-        for (int j = 0; j < w_u; ++j) {
-          const int s_j = __shfl_sync(0xffffffffu, slot_j, j);
-          const __nv_bfloat16 *src =
-              p.q + ((size_t)s_j * (kGroup * p.h_local) + x.g * kGroup) * kHeadDim;
-          if (elect_one()) bulk_g2s(smem + kOffQS + j * 2048, src, 2048, qs_full);
+        for (int j0 = 0; j0 < w_u; j0 += kQSRows / 8, ++qs_pass) {
+          const int nj = min(kQSRows / 8, w_u - j0);
+          mbar_wait(qs_free, (qs_pass & 1) ^ 1);
+          if (elect_one()) mbar_arrive_expect_tx(qs_full, nj * 2048);
           __syncwarp();
+          for (int j = 0; j < nj; ++j) {
+            const int s_j = __shfl_sync(0xffffffffu, slot_j, j0 + j);
+            const __nv_bfloat16 *src =
+                p.q + ((size_t)s_j * (kGroup * p.h_local) + x.g * kGroup) * kHeadDim;
+            if (elect_one()) bulk_g2s(smem + kOffQS + j * 2048, src, 2048, qs_full);
+            __syncwarp();
+          }
         }
       }
       int my_tok0 = 0, my_valid = 0, my_pg[kTile / 16] = {0, 0, 0, 0};
@@ -425,6 +438,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint8_t *dst = ring + st * kStageBytes;
         mbar_wait(ring_empty + st, ((n_prod / n_stages) & 1) ^ 1);
         if (is_k && lane == 0) trace_ev(p, 0, n_prod);
+        if (is_k && lane == 0 && p.trace != nullptr && t == 0 && n_prod == 0) {
+          unsigned long long g;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+          p.trace[(size_t)(3000 + blockIdx.x) * 16 + 2] = (long long)g;  // first TMA issued
+        }
         if (elect_one()) {
           if (p.tma5d) {
             // one box: {64 d, 64 tokens, 2 d-halves} -> [d-half][token][64] (two SW128 atoms)
@@ -513,12 +531,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int mrow = wq * 32 + lane;    // M-row (TMEM lane) owned by this thread
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
     const float c_log2 = p.scale_log2;
+    uint32_t qs_pass = 0;
     uint32_t n = 0;
     int it = ring_item(it_full, it_ring, 0);
     if (it >= 0) {
       Item x0;
       decode_item(p, it, x0);
-      stage_q_tmem(x0, smem + kOffQS, qs_full, qs_free, 0, tmem, lane_off, mrow);
+      stage_q_tmem(x0, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, mrow);
       mbar_arrive(q_full);
     }
     for (uint32_t item_idx = 0; it >= 0; ++item_idx) {
@@ -562,7 +581,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (next >= 0) {
         Item xn;
         decode_item(p, next, xn);
-        stage_q_tmem(xn, smem + kOffQS, qs_full, qs_free, item_idx + 1, tmem, lane_off, mrow);
+        stage_q_tmem(xn, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, mrow);
         mbar_arrive(q_full);
       }
       // publish (m, l) for the epilogue warps; xml[ob] was consumed by epilogue item_idx-2
@@ -610,36 +629,36 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const size_t prow = ((size_t)(x.cs0 + (i >> 3)) * h + x.g) * kGroup + (i & 7);
         p.part_lse[prow] = L > 0.f ? (M + __log2f(L)) * 0.69314718055994531f : -INFINITY;
       }
-      // four 32-column passes: every copy stages its scaled O row in SMEM, then all 128
+      // 16-column passes: every copy stages its scaled O row slice in SMEM, then all 128
       // threads sum the copies and write the rows with coalesced stores
+      constexpr int kF4 = kXCols / 4;  // float4 per row slice
 #pragma unroll 1
-      for (int half = 0; half < 4; ++half) {
+      for (int pass = 0; pass < kHeadDim / kXCols; ++pass) {
         if (warp_out) {
-          uint32_t o[32];
-          tmem_ld32(tO + half * 32, o);
+          uint32_t o[16];
+          tmem_ld16(tO + pass * kXCols, o);
           tmem_ld_wait();
           if (out_row) {
             float4 *xr = reinterpret_cast<float4 *>(xo + mrow * kXStride);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < kF4; ++j)
               xr[j] = make_float4(__uint_as_float(o[4 * j]) * f, __uint_as_float(o[4 * j + 1]) * f,
                                   __uint_as_float(o[4 * j + 2]) * f,
                                   __uint_as_float(o[4 * j + 3]) * f);
           }
         }
         named_bar_sync(2, 128);
-        for (int k = etid; k < R8 * 8; k += 128) {
-          const int row = k >> 3, c4 = k & 7;
+        for (int k = etid; k < R8 * kF4; k += 128) {
+          const int row = k / kF4, c4 = k % kF4;
           float4 a = reinterpret_cast<const float4 *>(xo + row * kXStride)[c4];
           for (int cc = 1; cc < rep; ++cc) {
             const float4 b = reinterpret_cast<const float4 *>(xo + (cc * rpc + row) * kXStride)[c4];
             a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
           }
           const size_t prow = ((size_t)(x.cs0 + (row >> 3)) * h + x.g) * kGroup + (row & 7);
-          reinterpret_cast<float4 *>(p.part_o + prow * kHeadDim + half * kXCols)[c4] = a;
+          reinterpret_cast<float4 *>(p.part_o + prow * kHeadDim + pass * kXCols)[c4] = a;
         }
-        if (warp == 8 && lane == 0 && half == 0) trace_ev(p, 13, 2048 + item_idx);
-        named_bar_sync(2, 128);  // staging reused by the next half / item
+        named_bar_sync(2, 128);  // staging reused by the next pass / item
       }
       if (warp == 6 && lane == 0) trace_ev(p, 14, 2048 + item_idx);
       if (warp == 8 && lane == 0) trace_ev(p, 15, 2048 + item_idx);
@@ -653,6 +672,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
+  }
+  if (p.trace != nullptr && tid == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    p.trace[(size_t)(3000 + blockIdx.x) * 16 + 1] = (long long)g;
   }
 }
 
@@ -673,54 +697,54 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
   // the attend kernel of this call has finished (stream order): re-arm its work counter
   if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<int32_t *>(p.hdr)[8] = 0;
   const int h = p.h_local;
-  const int n_items = __ldg(p.hdr + 2) * h;
+  const int n_rows = __ldg(p.hdr + 2) * h * kGroup;  // (admitted slot, KV head, GQA row)
   const int qheads = kGroup * h;
   const int warps = gridDim.x * (kMergeThreads / 32);
-  for (int it = blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5); it < n_items;
-       it += warps) {
-    const int k = it / h, g = it - k * h;
+  // one warp per output row: lane owns 4 of the 128 dims; single-pass online LSE merge of
+  // the row's partials (prefix chunks in order, then local items) with batched loads
+  for (int it = blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5); it < n_rows; it += warps) {
+    const int a = it % kGroup, kg = it / kGroup;
+    const int k = kg / h, g = kg - k * h;
     const int s = __ldg(p.adm_list + k);
     const int r = __ldg(p.slot_req + s);
     const int j = __ldg(p.slot_rank + s);
     const int w = __ldg(p.req_adm_off + r + 1) - __ldg(p.req_adm_off + r);
     const int nq = (__ldg(p.req_chunk_off + r + 1) - __ldg(p.req_chunk_off + r)) +
                    (__ldg(p.req_loc_off + r + 1) - __ldg(p.req_loc_off + r));
-    const int cs_base = __ldg(p.req_part_off + r) + j;
-    float M[kGroup], Z[kGroup], acc[kGroup][4];
+    const size_t row0 = ((size_t)(__ldg(p.req_part_off + r) + j) * h + g) * kGroup + a;
+    const size_t qstride = (size_t)w * h * kGroup;  // partial rows between items of r
+    float M = -INFINITY, Z = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q0 = 0; q0 < nq; q0 += 4) {
+      float l2[4];
+      float4 v[4];
 #pragma unroll
-    for (int a = 0; a < kGroup; ++a) {
-      M[a] = -INFINITY; Z[a] = 0.f;
-      acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
-    }
-    for (int q = 0; q < nq; ++q) {
-      const size_t prow0 = ((size_t)(cs_base + q * w) * h + g) * kGroup;
+      for (int u = 0; u < 4; ++u) {
+        const bool ok = q0 + u < nq;
+        const size_t prow = row0 + (size_t)(q0 + u) * qstride;
+        l2[u] = ok ? __ldg(p.part_lse + prow) * 1.4426950408889634f : -INFINITY;
+        v[u] = ok ? __ldg(reinterpret_cast<const float4 *>(p.part_o + prow * kHeadDim) + lane)
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-      for (int a = 0; a < kGroup; ++a)
-        M[a] = fmaxf(M[a], __ldg(p.part_lse + prow0 + a) * 1.4426950408889634f);
-    }
-    for (int q = 0; q < nq; ++q) {
-      const size_t prow0 = ((size_t)(cs_base + q * w) * h + g) * kGroup;
-#pragma unroll
-      for (int a = 0; a < kGroup; ++a) {
-        const float l2 = __ldg(p.part_lse + prow0 + a) * 1.4426950408889634f;
-        if (l2 == -INFINITY) continue;
-        const float wgt = ex2(l2 - M[a]);
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(p.part_o + (prow0 + a) * kHeadDim) + lane);
-        acc[a][0] += wgt * v.x; acc[a][1] += wgt * v.y; acc[a][2] += wgt * v.z; acc[a][3] += wgt * v.w;
-        Z[a] += wgt;
+      for (int u = 0; u < 4; ++u) {
+        if (l2[u] == -INFINITY) continue;
+        const float Mn = fmaxf(M, l2[u]);
+        const float sc = ex2(M - Mn), wgt = ex2(l2[u] - Mn);  // ex2(-inf) = 0
+        acc.x = acc.x * sc + wgt * v[u].x; acc.y = acc.y * sc + wgt * v[u].y;
+        acc.z = acc.z * sc + wgt * v[u].z; acc.w = acc.w * sc + wgt * v[u].w;
+        Z = Z * sc + wgt;
+        M = Mn;
       }
     }
-#pragma unroll
-    for (int a = 0; a < kGroup; ++a) {
-      const float inv = 1.f / Z[a];
-      __align__(8) __nv_bfloat162 o2[2];
-      o2[0] = __floats2bfloat162_rn(acc[a][0] * inv, acc[a][1] * inv);
-      o2[1] = __floats2bfloat162_rn(acc[a][2] * inv, acc[a][3] * inv);
-      *reinterpret_cast<uint2 *>(p.out + ((size_t)s * qheads + g * kGroup + a) * kHeadDim + 4 * lane) =
-          *reinterpret_cast<uint2 *>(o2);
-      if (p.lse_out && lane == a)
-        p.lse_out[(size_t)s * qheads + g * kGroup + a] = (M[a] + __log2f(Z[a])) * 0.69314718055994531f;
-    }
+    const float inv = 1.f / Z;
+    __align__(8) __nv_bfloat162 o2[2];
+    o2[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+    o2[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    *reinterpret_cast<uint2 *>(p.out + ((size_t)s * qheads + g * kGroup + a) * kHeadDim + 4 * lane) =
+        *reinterpret_cast<uint2 *>(o2);
+    if (p.lse_out && lane == 0)
+      p.lse_out[(size_t)s * qheads + g * kGroup + a] = (M + __log2f(Z)) * 0.69314718055994531f;
   }
 }
 
@@ -883,7 +907,7 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   mp.out = static_cast<__nv_bfloat16 *>(out);
   mp.lse_out = lse;
   mp.h_local = h;
-  int grid = (S * h + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
+  int grid = (S * h * kGroup + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
   if (grid > sms * 8) grid = sms * 8;
   merge_kernel<<<grid, kMergeThreads, 0, st>>>(mp);
   e = cudaGetLastError();

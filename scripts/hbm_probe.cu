@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <random>
 #include <cuda_runtime.h>
+#include <cuda.h>
 
 #include "../paper_2605_06914_b200/csrc/taper_internal.cuh"
 
@@ -119,6 +120,97 @@ void run_multi(const uint8_t *pool, const int *order, int n_pages, int page_byte
          (double)n_pages * page_bytes / (ms * 1e-3) / 1e9);
 }
 
+// Tensor-map TMA: P producer warps, each loading {64 d, 64 tok, 2 halves} 16 KB boxes of a
+// [pages, 1 head, 64 tok, 128 d] pool (the attention kernel's 5-D map), SW128.
+template <int STAGES, int P, bool FIVE_D>
+__global__ void __launch_bounds__(64 * P, 1) tensor_probe(const __grid_constant__ CUtensorMap tm,
+                                                          const int *order, int n_pages,
+                                                          unsigned long long *sink) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t full[P][STAGES], empty[P][STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pid = warp % P, role = warp / P;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < P; ++q)
+      for (int i = 0; i < STAGES; ++i) { mbar_init(&full[q][i], 1); mbar_init(&empty[q][i], 1); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint8_t *ring = smem + pid * STAGES * 16384;
+  if (lane == 0) {
+    unsigned long long acc = 0;
+    int n = 0;
+    for (long long c = blockIdx.x * P + pid; c < n_pages; c += (long long)gridDim.x * P, ++n) {
+      const int st = n % STAGES;
+      if (role == 0) {
+        mbar_wait(&empty[pid][st], ((n / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[pid][st], 16384);
+        const int page = order[c] % n_pages;
+        if (FIVE_D) {
+          tma_load_5d(ring + st * 16384, &tm, &full[pid][st], 0, 0, 0, 0, page);
+        } else {
+          tma_load_4d(ring + st * 16384, &tm, &full[pid][st], 0, 0, 0, page);
+          tma_load_4d(ring + st * 16384 + 8192, &tm, &full[pid][st], 64, 0, 0, page);
+        }
+      } else {
+        mbar_wait(&full[pid][st], (n / STAGES) & 1);
+        acc += ring[st * 16384 + (n & 127)];
+        mbar_arrive(&empty[pid][st]);
+      }
+    }
+    if (acc == 0xdeadbeef) *sink = acc;
+  }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                             const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                             const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+template <int STAGES, int P, bool FIVE_D>
+void run_tensor(void *pool, const int *order, int n_pages, unsigned long long *sink, int sms,
+                CUtensorMapL2promotion promo) {
+  void *fp = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
+  EncodeFn enc = reinterpret_cast<EncodeFn>(fp);
+  CUtensorMap tm;
+  CUresult r;
+  if (FIVE_D) {
+    cuuint64_t dims[5] = {64, 64, 2, 1, (cuuint64_t)n_pages};
+    cuuint64_t strides[4] = {256, 128, 256 * 64, 256 * 64};
+    cuuint32_t box[5] = {64, 64, 2, 1, 1}, es[5] = {1, 1, 1, 1, 1};
+    r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, pool, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[4] = {128, 64, 1, (cuuint64_t)n_pages};
+    cuuint64_t strides[3] = {256, 256 * 64, 256 * 64};
+    cuuint32_t box[4] = {64, 64, 1, 1}, es[4] = {1, 1, 1, 1};
+    r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, pool, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) { printf("encode failed %d\n", int(r)); return; }
+  auto k = tensor_probe<STAGES, P, FIVE_D>;
+  const int smem = P * STAGES * 16384 + 1024;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(a);
+    k<<<sms, 64 * P, smem>>>(tm, order, n_pages, sink);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+  }
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  printf("tensor TMA %s %d producers stages=%d promo=%d: %7.1f GB/s %s\n", FIVE_D ? "5D 16KB box" : "4D 2x8KB",
+         P, STAGES, int(promo), (double)n_pages * 16384 / (ms * 1e-3) / 1e9,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
 __global__ void ldg_probe(const uint4 *pool, const int *order, int n_pages, int page_bytes,
                           unsigned long long *sink) {
   const int per_page = page_bytes / 16;
@@ -196,6 +288,11 @@ int main() {
   run_multi<3, 16384, 4>(pool, order, n_pages, page_bytes, sink, sms);
   run_multi<6, 8192, 4>(pool, order, n_pages, page_bytes, sink, sms);
   run_multi<3, 8192, 8>(pool, order, n_pages, page_bytes, sink, sms);
+  run_tensor<5, 2, true>(pool, order, n_pages, sink, sms, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  run_tensor<5, 2, true>(pool, order, n_pages, sink, sms, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+  run_tensor<3, 4, true>(pool, order, n_pages, sink, sms, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  run_tensor<5, 2, false>(pool, order, n_pages, sink, sms, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  run_tensor<3, 4, false>(pool, order, n_pages, sink, sms, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
   printf("sequential pages:\n");
   run_tma<8, 16384>(pool, seq, n_pages, page_bytes, sink, sms, 1);
   run_tma<4, 16384>(pool, seq, n_pages, page_bytes, sink, sms, 4);

@@ -16,6 +16,7 @@ EV = ["tma_issue", "mma_full", "qk_commit", "pv_pfull", "pv_ofree", "pv_commit",
 
 
 def main():
+    global _fn
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
     b = synth.config_batch(cfg, seed=0)
     lay = synth.make_layout(b, 64, np.random.default_rng(1), 1)
@@ -34,7 +35,7 @@ def main():
     out = torch.empty_like(q)
     for _ in range(3):
         T.taper_decode_attention(db, adm, kv, q, out, None, 1 / math.sqrt(128), ws)
-    cap = 4096
+    cap = 3200
     tr = torch.zeros(cap * 16, dtype=torch.int64, device="cuda")
     T.taper_set_trace_buffer(tr, cap)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -43,7 +44,14 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     T.taper_set_trace_buffer(None)
+    clocks_under_load(lambda: T.taper_decode_attention(db, adm, kv, q, out, None,
+                                                         1 / math.sqrt(128), ws))
     print(f"layer time {e0.elapsed_time(e1) * 1e3:.1f} us")
+    cta = tr.view(cap, 16).cpu().numpy()[3000:3000 + 148, :3].astype(np.int64)
+    g0 = cta[:, 0].min()
+    print("per-CTA (us): start min/max %.1f/%.1f, first TMA median %.1f, end min/median/max %.1f/%.1f/%.1f" % (
+        (cta[:, 0].min() - g0) / 1e3, (cta[:, 0].max() - g0) / 1e3, np.median(cta[:, 2] - g0) / 1e3,
+        (cta[:, 1].min() - g0) / 1e3, np.median(cta[:, 1] - g0) / 1e3, (cta[:, 1].max() - g0) / 1e3))
     a = tr.view(cap, 16).cpu().numpy()
     n = int((a[:, 1] > 0).sum())
     a = a[:n].astype(np.int64)
@@ -75,9 +83,34 @@ def main():
         r = a[i]
         print(i, r[15], r[0] - r[15], r[12] - r[0], r[13] - r[12], r[14] - r[13], "next top", a[i + 1][15] - r[14])
     print("first 40 tiles (cycles rel.):")
+    FIRST40 = True
     print("   n " + " ".join(f"{e[:9]:>9s}" for e in EV))
     for i in range(min(40, n)):
         print(f"{i:4d} " + " ".join(f"{x:9d}" for x in a[i, :12]))
+
+
+def clocks_under_load(fn, seconds=3.0):
+    """Run fn() back to back for ~seconds while sampling nvidia-smi every 50 ms."""
+    import subprocess, time
+    q = ("clocks.sm,clocks.mem,power.draw,clocks_event_reasons.sw_power_cap,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.hw_power_brake_slowdown,temperature.gpu")
+    proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                             "-lms", "50", "-i", "0"], stdout=subprocess.PIPE, text=True)
+    time.sleep(0.3)
+    t_end = time.time() + seconds
+    n = 0
+    while time.time() < t_end:
+        for _ in range(20):
+            fn()
+        n += 20
+    torch.cuda.synchronize()
+    time.sleep(0.2)
+    proc.terminate()
+    lines = proc.stdout.read().strip().splitlines()
+    print(f"{n} launches; nvidia-smi samples (sm MHz, mem MHz, W, pwr_cap, hw_slow, sw_therm, pwr_brake, C):")
+    for ln in lines[len(lines) // 3: len(lines) // 3 + 12]:
+        print("   ", ln)
 
 
 if __name__ == "__main__":
