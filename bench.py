@@ -340,6 +340,13 @@ def run_ours(args):
     by = algorithmic_bytes(batch, adm_mask, h)
     sh_avg = float(np.mean([p[l][0].elapsed_time(p[l][1]) for p in prof for l in range(L)]))
     lo_avg = float(np.mean([p[l][1].elapsed_time(p[l][2]) for p in prof for l in range(L)]))
+    traffic = None  # dram read+write bytes per launch from the committed ncu capture
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "attend_traffic.json")))
+        if tj.get("workload") == args.config and h == 8:
+            traffic = tj["bytes_per_launch"]
+    except Exception:
+        pass
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -386,7 +393,9 @@ def run_ours(args):
                           "admit_and_collectives_per_step":
                               ms_per_step * 1e3 - L * (sh_avg + lo_avg) * 1e3},
             "roofline": {"bound": "hbm", "achieved": sh_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": sh_gbs / hbm_peak, "traffic": None,
+                         "frac": sh_gbs / hbm_peak, "traffic": traffic,
+                         "traffic_source": "profiles/attend_traffic.json (ncu --set full)"
+                         if traffic else None,
                          "kernel": "attend_kernel",
                          "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                          "bytes_per_launch": by["attend_kernel"]},
