@@ -355,7 +355,10 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     if (w == 0) continue;
     const int adm_off = p.req_adm_off[r];
     const int nr = p.off[r + 1] - p.off[r];
-    const int rep = (8 * nr <= 32) ? 4 : ((8 * nr <= 64) ? 2 : 1);
+    // <= 8 ready branches: M = 64 MMAs (16 rows per TMEM lane quadrant), replicated 4 / 2 / 1
+    // times for <= 16 / 32 / 64 stacked rows; else M = 128 without replication
+    const int m64 = (8 * nr <= 64) ? 1 : 0;
+    const int rep = m64 ? ((8 * nr <= 16) ? 4 : ((8 * nr <= 32) ? 2 : 1)) : 1;
     const int nc = p.req_chunk_off[r + 1] - p.req_chunk_off[r];
     const int cs_r = p.req_part_off[r];
     for (int c = 0; c < nc; ++c) {
@@ -363,8 +366,8 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       d.r = r; d.w = w; d.adm_off = adm_off; d.cs0 = cs_r + c * w;
       d.tb = c * kChunk; d.te = min(d.tb + kChunk, p.Lsh[r]);
       d.nt = (d.te - d.tb + kTileTokens - 1) / kTileTokens;
-      d.flags = rep << 1;
-      p.items[p.req_chunk_off[r] + c] = d;
+      d.flags = (rep << 1) | (m64 << 4);
+      p.items[p.req_chunk_off[r] + p.req_loc_off[r] + c] = d;  // request-major numbering
     }
     // local tiles of the admitted branches, branch-major, grouped 16 per local item
     const int l0 = p.req_loc_off[r], nl = p.req_loc_off[r + 1] - l0;
@@ -381,8 +384,8 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       d.r = r; d.w = w; d.adm_off = adm_off; d.cs0 = cs_r + (nc + li) * w;
       d.tb = (l0 + li) * kLocalItemTiles; d.te = 0;
       d.nt = min(kLocalItemTiles, lt - li * kLocalItemTiles);
-      d.flags = 1 | (rep << 1);
-      p.items[tot_nc + l0 + li] = d;
+      d.flags = 1 | (rep << 1) | (m64 << 4);
+      p.items[p.req_chunk_off[r] + l0 + nc + li] = d;
     }
   }
   // adm_list: ascending slot index

@@ -65,6 +65,8 @@ constexpr uint32_t kColQ = 384;   // Q [384, 448): 128 bf16 per row as 64 packed
 
 constexpr uint32_t kIdescQK = umma_idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, false, true);
+constexpr uint32_t kIdescQK64 = umma_idesc_bf16(64, 64, false, false);
+constexpr uint32_t kIdescPV64 = umma_idesc_bf16(64, 128, false, true);
 
 struct AttnParams {
   const int32_t *slot_page_off, *slot_pages, *req_page_off, *req_pages;
@@ -87,8 +89,16 @@ __device__ __forceinline__ void trace_ev(const AttnParams &p, int e, uint32_t n)
 }
 
 struct Item {
-  int r, g, local, w, adm_off, cs0, nt, tb, te, rep;
+  int r, g, local, w, adm_off, cs0, nt, tb, te, rep, m64;
 };
+
+// TMEM row layout of the MMA accumulator (cta_group::1): M = 128 puts row m in lane m; M = 64
+// puts rows 16q..16q+15 in lanes 32q..32q+15 (16 rows per lane quadrant).  Returns the M-row
+// held by (quadrant wq, lane) or -1.
+__device__ __forceinline__ int mrow_of(int m64, int wq, int lane) {
+  if (!m64) return wq * 32 + lane;
+  return lane < 16 ? wq * 16 + lane : -1;
+}
 
 __device__ __forceinline__ void decode_item(const AttnParams &p, int it, Item &x) {
   const int q = it / p.h_local;
@@ -98,7 +108,8 @@ __device__ __forceinline__ void decode_item(const AttnParams &p, int it, Item &x
   x.r = a.x; x.w = a.y; x.adm_off = a.z; x.cs0 = a.w;
   x.tb = b.x; x.te = b.y; x.nt = b.z;
   x.local = b.w & 1;
-  x.rep = b.w >> 1;
+  x.rep = (b.w >> 1) & 7;
+  x.m64 = (b.w >> 4) & 1;
 }
 
 struct TileInfo {
@@ -144,10 +155,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // complete and fenced.  `pass` counts staging passes consumed so far (updated).
 __device__ __forceinline__ void stage_q_tmem(const Item &x, const uint8_t *qs, uint64_t *qs_full,
                                              uint64_t *qs_free, uint32_t &pass, uint32_t tmem,
-                                             uint32_t lane_off, int mrow) {
+                                             uint32_t lane_off, int wq, int lane) {
   const int R8 = 8 * x.w;
-  const int rpc = 128 / x.rep;
-  const int i = mrow % rpc;
+  const int m = mrow_of(x.m64, wq, lane);
+  const int rpc = (x.m64 ? 64 : 128) / x.rep;
+  const int i = m >= 0 ? m % rpc : 1 << 20;
   uint32_t v[64];
 #pragma unroll
   for (int c = 0; c < 64; ++c) v[c] = 0u;
@@ -178,13 +190,13 @@ __device__ __forceinline__ bool elect_one() {
 
 // S[tS] = Q[tQ] * K^T: 8 k-steps of 16 over d = 128 (A = Q from TMEM, B = K tile in SMEM,
 // SW128 K-major: d 0..63 in the first 8 KB box, 64..127 in the second).
-__device__ __forceinline__ void issue_qk(uint32_t tS, uint32_t tQ, uint32_t kb) {
+__device__ __forceinline__ void issue_qk(uint32_t tS, uint32_t tQ, uint32_t kb, uint32_t idesc) {
   const uint32_t nomask[4] = {0u, 0u, 0u, 0u};
   const uint64_t b0 = umma_desc_sw128(kb, 16, 1024);
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     const uint64_t b = b0 + uint64_t((((kk >> 2) * 8192) + (kk & 3) * 32) >> 4);
-    tc_mma_f16_ts(tS, tQ + kk * 8, b, kIdescQK, kk > 0 ? 1u : 0u, nomask);
+    tc_mma_f16_ts(tS, tQ + kk * 8, b, idesc, kk > 0 ? 1u : 0u, nomask);
   }
 }
 
@@ -193,7 +205,8 @@ __device__ __forceinline__ void issue_qk(uint32_t tS, uint32_t tQ, uint32_t kb) 
 // replicated row copies, copy c owns tokens [c*64/REP, (c+1)*64/REP): its k-steps run
 // with the other copies' TMEM lanes masked off.
 template <int REP>
-__device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t vb, bool first) {
+__device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t vb, bool first,
+                                         uint32_t idesc) {
   const uint64_t b0 = umma_desc_sw128(vb, 8192, 1024);
   constexpr int KPC = 4 / REP;
 #pragma unroll
@@ -208,7 +221,7 @@ __device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t vb, 
       for (int k = 0; k < KPC; ++k) {
         const int kk = c * KPC + k;
         const uint64_t b = b0 + uint64_t((kk * 2048) >> 4);
-        tc_mma_f16_ts(tO, tP + part * 32 + kk * 8, b, kIdescPV,
+        tc_mma_f16_ts(tO, tP + part * 32 + kk * 8, b, idesc,
                       (first && part == 0 && k == 0) ? 0u : 1u, mask);
       }
     }
@@ -479,6 +492,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       Item x;
       decode_item(p, it, x);
       const int rep = __shfl_sync(0xffffffffu, x.rep, 0);
+      const int m64 = __shfl_sync(0xffffffffu, x.m64, 0);
+      const uint32_t idesc_qk = m64 ? kIdescQK64 : kIdescQK;
+      const uint32_t idesc_pv = m64 ? kIdescPV64 : kIdescPV;
       const uint32_t ob = item_idx & 1;  // O double buffer
       const uint32_t tO = tmem_u + kColO + ob * 128;
       mbar_wait(q_full, item_idx & 1);
@@ -491,7 +507,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           if (lane == 0) trace_ev(p, 1, n);
           tc_fence_after();
           if (elect_one()) {
-            issue_qk(tmem_u + kColS + (n & 1) * 64, tmem_u + kColQ, sK + ks * kStageBytes);
+            issue_qk(tmem_u + kColS + (n & 1) * 64, tmem_u + kColQ, sK + ks * kStageBytes, idesc_qk);
             tc_commit(kempty + ks);
             tc_commit(s_full + (n & 1));
           }
@@ -512,9 +528,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           if (elect_one()) {
             const uint32_t tP = tmem_u + kColS + (m & 1) * 64;
             const uint32_t vb = sV + vs * kStageBytes;
-            if (rep == 4) issue_pv<4>(tO, tP, vb, first);
-            else if (rep == 2) issue_pv<2>(tO, tP, vb, first);
-            else issue_pv<1>(tO, tP, vb, first);
+            if (rep == 4) issue_pv<4>(tO, tP, vb, first, idesc_pv);
+            else if (rep == 2) issue_pv<2>(tO, tP, vb, first, idesc_pv);
+            else issue_pv<1>(tO, tP, vb, first, idesc_pv);
             tc_commit(vempty + vs);
             tc_commit(pv_done + (m & 1));
             if (t == x.nt) tc_commit(o_full + ob);
@@ -528,7 +544,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   } else if (warp < 6) {
     // ======================= softmax / O correction (128 threads) =======================
     const int wq = warp & 3;            // TMEM lane quadrant of this warp
-    const int mrow = wq * 32 + lane;    // M-row (TMEM lane) owned by this thread
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
     const float c_log2 = p.scale_log2;
     uint32_t qs_pass = 0;
@@ -537,7 +552,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (it >= 0) {
       Item x0;
       decode_item(p, it, x0);
-      stage_q_tmem(x0, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, mrow);
+      stage_q_tmem(x0, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, wq, lane);
       mbar_arrive(q_full);
     }
     for (uint32_t item_idx = 0; it >= 0; ++item_idx) {
@@ -545,8 +560,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       decode_item(p, it, x);
       const int R8 = 8 * x.w;
       const int rep = x.rep;
-      const int rpc = 128 / rep, cw = 64 / rep;
-      const int copy = mrow / rpc, i = mrow - copy * rpc;
+      const int mrow = mrow_of(x.m64, wq, lane);  // M-row held by this thread, -1: none
+      const int rpc = (x.m64 ? 64 : 128) / rep, cw = 64 / rep;
+      const int copy = mrow >= 0 ? mrow / rpc : 0;
+      const int i = mrow >= 0 ? mrow - copy * rpc : 1 << 20;  // stacked row (dead if >= R8)
       const int colbase = copy * cw;
       const uint32_t ob = item_idx & 1;
       const uint32_t tO = tmem + lane_off + kColO + ob * 128;
@@ -581,12 +598,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (next >= 0) {
         Item xn;
         decode_item(p, next, xn);
-        stage_q_tmem(xn, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, mrow);
+        stage_q_tmem(xn, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, wq, lane);
         mbar_arrive(q_full);
       }
       // publish (m, l) for the epilogue warps; xml[ob] was consumed by epilogue item_idx-2
       mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);
-      xml[ob * 128 + mrow] = make_float2(m_run, l_run);
+      if (mrow >= 0) xml[ob * 128 + mrow] = make_float2(m_run, l_run);
       mbar_arrive(ml_full + ob);
       it = next;
     }
@@ -595,7 +612,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // Merges the replicated copies of each stacked row and writes the normalised partial
     // (o, lse), overlapping the next item's tiles (O is double-buffered in TMEM).
     const int wq = warp & 3;
-    const int mrow = wq * 32 + lane;
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
     for (uint32_t item_idx = 0;; ++item_idx) {
       const int it = ring_item(it_full, it_ring, item_idx);
@@ -605,24 +621,29 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       decode_item(p, it, x);
       const int R8 = 8 * x.w;
       const int rep = x.rep;
-      const int rpc = 128 / rep;
-      const int copy = mrow / rpc, i = mrow - copy * rpc;
+      const int mrow = mrow_of(x.m64, wq, lane);
+      const int rpc = (x.m64 ? 64 : 128) / rep;
+      const int copy = mrow >= 0 ? mrow / rpc : 0;
+      const int i = mrow >= 0 ? mrow - copy * rpc : 1 << 20;
       const uint32_t ob = item_idx & 1;
       const uint32_t tO = tmem + lane_off + kColO + ob * 128;
       mbar_wait(ml_full + ob, (item_idx >> 1) & 1);
       mbar_wait(o_full + ob, (item_idx >> 1) & 1);
       if (warp == 6 && lane == 0) trace_ev(p, 10, 2048 + item_idx);
       tc_fence_after();
-      const float2 mine = xml[ob * 128 + mrow];
+      const bool has = mrow >= 0 && i < R8;
+      const float2 mine = has ? xml[ob * 128 + mrow] : make_float2(-INFINITY, 0.f);
       float M = -INFINITY, L = 0.f;
-      for (int c = 0; c < rep; ++c) M = fmaxf(M, xml[ob * 128 + c * rpc + i].x);
-      for (int c = 0; c < rep; ++c) {
-        const float2 ml = xml[ob * 128 + c * rpc + i];
-        if (ml.y > 0.f) L += ex2(ml.x - M) * ml.y;
+      if (has) {
+        for (int c = 0; c < rep; ++c) M = fmaxf(M, xml[ob * 128 + c * rpc + i].x);
+        for (int c = 0; c < rep; ++c) {
+          const float2 ml = xml[ob * 128 + c * rpc + i];
+          if (ml.y > 0.f) L += ex2(ml.x - M) * ml.y;
+        }
       }
       const float f = (L > 0.f && mine.y > 0.f) ? ex2(mine.x - M) / L : 0.f;
       if (warp == 6 && lane == 0) trace_ev(p, 12, 2048 + item_idx);
-      const bool out_row = i < R8;
+      const bool out_row = has;
       const bool warp_out = __any_sync(0xffffffffu, out_row);
       const int etid = tid - 192;  // 0..127
       if (out_row && copy == 0) {

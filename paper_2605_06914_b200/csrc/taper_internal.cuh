@@ -59,7 +59,7 @@ constexpr size_t kLocalTileBytes = 16;                // int4 {slot, tok0, valid
 constexpr size_t kWorkBytesPerCs = kItemDescBytes + kLocalItemTiles * kLocalTileBytes;
 
 // Work item descriptor emitted by the admission kernel (A5).  Items are numbered per KV
-// head: prefix chunks of all requests first (request-major), then local items.
+// head, request-major: request r's prefix chunks, then its local items.
 struct ItemDesc {
   int32_t r;        // request
   int32_t w;        // admitted branches (stacked rows = 8 w)
