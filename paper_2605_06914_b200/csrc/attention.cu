@@ -229,14 +229,25 @@ __device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t vb, 
 }
 
 // One tile of the online softmax for a thread's row, branch-free.  CW = tokens of the tile
-// owned by this row's copy; nvalid = live tokens among them (0 for a row that is dead in
-// this tile).  Updates m_run / l_run and writes P (hi, lo) into the row's S columns.
-template <int CW>
+// handled by this thread; nvalid = live tokens among them (0 for a row that is dead in this
+// tile).  Updates m_run and this thread's share of l_run, and writes P (hi, lo) into the
+// row's S columns.  M = 128 (SPLIT = false): one thread per row (TMEM lane), tokens
+// [colbase, colbase + CW).  M = 64 (SPLIT = true): rows live in lanes 0-15 of the quadrant and
+// two threads share a row -- lane t < 16 takes tokens [colbase, +CW), lane t + 16 the next CW
+// (16x32bx2 accesses); the row max is combined across the pair, the row sum at the end of
+// the item.
+template <int CW, bool SPLIT>
 __device__ __forceinline__ void softmax_tile(uint32_t tS, int colbase, int nvalid, bool o_live,
                                              float c, float &m_run, float &l_run, uint32_t tO,
                                              uint64_t *pv_prev, uint32_t pv_prev_parity) {
   uint32_t s[CW];
-  tmem_ld_n<CW>(tS + colbase, s);
+  if constexpr (SPLIT) {
+    if constexpr (CW == 8) tmem_ld_x2_8<CW>(tS + colbase, s);
+    else if constexpr (CW == 16) tmem_ld_x2_16<CW>(tS + colbase, s);
+    else tmem_ld_x2_32<CW>(tS + colbase, s);
+  } else {
+    tmem_ld_n<CW>(tS + colbase, s);
+  }
   tmem_ld_wait();
   float x[CW];
 #pragma unroll
@@ -244,6 +255,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, int colbase, int nvali
   float mx = x[0];
 #pragma unroll
   for (int j = 1; j < CW; ++j) mx = fmaxf(mx, x[j]);
+  if constexpr (SPLIT) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
   mx *= c;  // scores in log2 units (c = softmax scale * log2 e > 0)
   // lazy rescale: only raise the running max when it grows by more than 8 (log2 units)
   const bool need = mx > m_run + 8.f;
@@ -257,26 +269,29 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, int colbase, int nvali
     mbar_wait(pv_prev, pv_prev_parity);  // O *= alpha needs PV(n-1) complete
     tc_fence_after();
 #pragma unroll 1
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < (SPLIT ? 2 : 4); ++q) {
       uint32_t o[32];
-      tmem_ld32(tO + q * 32, o);
+      if constexpr (SPLIT) tmem_ld_x2_32<64>(tO + q * 32, o);
+      else tmem_ld32(tO + q * 32, o);
       tmem_ld_wait();
 #pragma unroll
       for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-      tmem_st32(tO + q * 32, o);
+      if constexpr (SPLIT) tmem_st_x2_32<64>(tO + q * 32, o);
+      else tmem_st32(tO + q * 32, o);
     }
     tmem_st_wait();
   }
   // P = 2^(x - m) split into hi + lo bf16 (DESIGN.md Sec. 6 "P precision"), written back
-  // into this row's S columns in groups of 16 tokens (8 packed columns per part)
+  // into this row's S columns in groups of up to 16 tokens (8 packed columns per part)
+  constexpr int G = CW < 16 ? CW : 16;
   const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
   float lsum = 0.f;
 #pragma unroll
-  for (int g16 = 0; g16 < CW / 16; ++g16) {
-    uint32_t hi[8], lo[8];
+  for (int g = 0; g < CW / G; ++g) {
+    uint32_t hi[G / 2], lo[G / 2];
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      const int j = g16 * 8 + jj;
+    for (int jj = 0; jj < G / 2; ++jj) {
+      const int j = g * (G / 2) + jj;
       const float e0 = ex2(fmaf(x[2 * j], c, neg_m));
       const float e1 = ex2(fmaf(x[2 * j + 1], c, neg_m));
       lsum += e0 + e1;
@@ -286,8 +301,19 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, int colbase, int nvali
       hi[jj] = *reinterpret_cast<const uint32_t *>(&h2);
       lo[jj] = *reinterpret_cast<const uint32_t *>(&l2);
     }
-    tmem_st8(tS + colbase / 2 + g16 * 8, hi);
-    tmem_st8(tS + 32 + colbase / 2 + g16 * 8, lo);
+    const uint32_t col = colbase / 2 + g * (G / 2);
+    if constexpr (SPLIT) {
+      if constexpr (G == 8) {
+        tmem_st_x2_4<CW / 2>(tS + col, hi);
+        tmem_st_x2_4<CW / 2>(tS + 32 + col, lo);
+      } else {
+        tmem_st_x2_8<CW / 2>(tS + col, hi);
+        tmem_st_x2_8<CW / 2>(tS + 32 + col, lo);
+      }
+    } else {
+      tmem_st8(tS + col, hi);
+      tmem_st8(tS + 32 + col, lo);
+    }
   }
   l_run += lsum;
   tmem_st_wait();
@@ -560,11 +586,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       decode_item(p, it, x);
       const int R8 = 8 * x.w;
       const int rep = x.rep;
-      const int mrow = mrow_of(x.m64, wq, lane);  // M-row held by this thread, -1: none
-      const int rpc = (x.m64 ? 64 : 128) / rep, cw = 64 / rep;
-      const int copy = mrow >= 0 ? mrow / rpc : 0;
-      const int i = mrow >= 0 ? mrow - copy * rpc : 1 << 20;  // stacked row (dead if >= R8)
+      // M-row of this thread; M = 64 rows are shared by lane pairs (t, t + 16), half h
+      const int m64 = x.m64;
+      const int mrow = m64 ? wq * 16 + (lane & 15) : wq * 32 + lane;
+      const int h = m64 ? lane >> 4 : 0;
+      const int rpc = (m64 ? 64 : 128) / rep, cw = 64 / rep;
+      const int copy = mrow / rpc;
+      const int i = mrow - copy * rpc;  // stacked row (dead if >= R8)
       const int colbase = copy * cw;
+      const int tw = m64 ? cw / 2 : cw;  // tokens handled by this thread
+      const int tok0 = colbase + h * tw;
       const uint32_t ob = item_idx & 1;
       const uint32_t tO = tmem + lane_off + kColO + ob * 128;
       float m_run = -INFINITY, l_run = 0.f;
@@ -572,7 +603,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const uint32_t sb = n & 1;
         const int2 tr = tile_rows(p, x, t);  // {valid tokens, owning branch or -1}
         const bool live = i < R8 && (tr.y < 0 || (i >> 3) == tr.y);
-        const int nvalid = live ? max(0, min(cw, tr.x - colbase)) : 0;
+        const int nvalid = live ? max(0, min(tw, tr.x - tok0)) : 0;
         mbar_wait(s_full + sb, (n >> 1) & 1);
         if (warp == 2 && lane == 0) trace_ev(p, 7, n);
         tc_fence_after();
@@ -581,17 +612,27 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint64_t *pv_prev = pv_done + ((n - 1) & 1);
         const uint32_t pv_par = ((n - 1) >> 1) & 1;
         const bool o_live = t > 0;
-        if (cw == 16)
-          softmax_tile<16>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
-        else if (cw == 32)
-          softmax_tile<32>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
-        else
-          softmax_tile<64>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
+        if (m64) {
+          if (cw == 16)
+            softmax_tile<8, true>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
+          else if (cw == 32)
+            softmax_tile<16, true>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
+          else
+            softmax_tile<32, true>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
+        } else {
+          if (cw == 16)
+            softmax_tile<16, false>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
+          else if (cw == 32)
+            softmax_tile<32, false>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
+          else
+            softmax_tile<64, false>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
+        }
         tc_fence_before();
         if (lane == 0) trace_ev(p, warp == 2 ? 8 : 6 + warp, n);  // warps 3,4,5 -> 9,10,11
         mbar_arrive(p_full + sb);
         ++n;
       }
+      if (m64) l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);  // row sum of the lane pair
       // all QK MMAs of this item are complete -> stage the next item's queries
       const int next = ring_item(it_full, it_ring, item_idx + 1);
       ring_release(it_empty, item_idx, lane);
@@ -603,7 +644,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       // publish (m, l) for the epilogue warps; xml[ob] was consumed by epilogue item_idx-2
       mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);
-      if (mrow >= 0) xml[ob * 128 + mrow] = make_float2(m_run, l_run);
+      if (h == 0) xml[ob * 128 + mrow] = make_float2(m_run, l_run);
       mbar_arrive(ml_full + ob);
       it = next;
     }

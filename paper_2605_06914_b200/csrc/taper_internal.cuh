@@ -68,7 +68,7 @@ struct ItemDesc {
   int32_t tb;       // prefix chunk: first token; local item: first local-tile entry
   int32_t te;       // prefix chunk: end token;   local item: unused
   int32_t nt;       // 64-token tiles
-  int32_t flags;    // bit 0: local item; bits 1..: replication factor (1, 2, 4)
+  int32_t flags;    // bit 0: local item; bits 1-3: replication factor (1, 2, 4); bit 4: M = 64
 };
 
 __host__ __device__ inline int64_t ws_cap_cs(size_t bytes, int R, int S, int h_local) {
@@ -282,6 +282,56 @@ __device__ __forceinline__ void tmem_st_n(uint32_t taddr, const uint32_t *v) {
       tmem_st32(taddr + 32 * i, *reinterpret_cast<const uint32_t(*)[32]>(v + 32 * i));
   }
 }
+// 16 lanes, two threads per lane ("16x32bx2"): thread t < 16 reads / writes lane t columns
+// [taddr + j], thread t >= 16 lane t - 16 columns [taddr + IMM + j], j < N.  Used for M = 64
+// accumulators, whose rows live in lanes 0-15 of each quadrant.
+#define TAPER_X2_LD(N, ADDR, IMMOP, REGS, ...)                                                 \
+  template <int IMM>                                                                           \
+  __device__ __forceinline__ void tmem_ld_x2_##N(uint32_t taddr, uint32_t *v) {                \
+    asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x" #N ".b32 {" REGS "}, [" ADDR "], " IMMOP \
+                 ";"                                                                           \
+                 : __VA_ARGS__                                                                 \
+                 : "r"(taddr), "n"(IMM));                                                      \
+  }
+#define TAPER_O4(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3])
+TAPER_X2_LD(8, "%8", "%9", "%0,%1,%2,%3,%4,%5,%6,%7", TAPER_O4(0), TAPER_O4(4))
+TAPER_X2_LD(16, "%16", "%17", "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15", TAPER_O4(0),
+            TAPER_O4(4), TAPER_O4(8), TAPER_O4(12))
+TAPER_X2_LD(32, "%32", "%33",
+            "%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,"
+            "%23,%24,%25,%26,%27,%28,%29,%30,%31",
+            TAPER_O4(0), TAPER_O4(4), TAPER_O4(8), TAPER_O4(12), TAPER_O4(16), TAPER_O4(20),
+            TAPER_O4(24), TAPER_O4(28))
+#undef TAPER_O4
+#undef TAPER_X2_LD
+template <int IMM>
+__device__ __forceinline__ void tmem_st_x2_4(uint32_t taddr, const uint32_t *v) {
+  asm volatile("tcgen05.st.sync.aligned.16x32bx2.x4.b32 [%0], %1, {%2,%3,%4,%5};" ::"r"(taddr),
+               "n"(IMM), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+template <int IMM>
+__device__ __forceinline__ void tmem_st_x2_8(uint32_t taddr, const uint32_t *v) {
+  asm volatile("tcgen05.st.sync.aligned.16x32bx2.x8.b32 [%0], %1, {%2,%3,%4,%5,%6,%7,%8,%9};" ::"r"(
+                   taddr),
+               "n"(IMM), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
+               "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+template <int IMM>
+__device__ __forceinline__ void tmem_st_x2_32(uint32_t taddr, const uint32_t *v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x32bx2.x32.b32 [%0], %1, {%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33};" ::"r"(
+          taddr),
+      "n"(IMM), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),
+      "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]),
+      "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]),
+      "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int n_threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n_threads) : "memory");
 }
