@@ -40,28 +40,31 @@ constexpr int kTile = kTileTokens;   // 64 tokens per pipeline stage
 // K and V tiles ride separate TMA rings: a K stage is released as soon as QK(t) completes,
 // a V stage only after PV(t); each stage is 64 tokens x 128 d bf16 = two 8 KB boxes.
 constexpr int kKStages = 6;
-constexpr int kVStages = 5;
+constexpr int kVStages = 6;
 constexpr int kStageBytes = 2 * 8192;
 constexpr int kOffV = kKStages * kStageBytes;                 // 64 KB
 constexpr int kOffQS = kOffV + kVStages * kStageBytes;        // 160 KB: next item's queries
 constexpr int kQSRows = 64;                                   // staged rows per pass
-constexpr int kQSBytes = kQSRows * 256;                       // 64 rows x 128 bf16
+constexpr int kQSStride = 256 + 16;  // padded row stride: conflict-free 16 B row reads
+constexpr int kQSBytes = kQSRows * kQSStride;                 // 64 rows x 128 bf16
 constexpr int kXCols = 16;                                    // epilogue pass width
 constexpr int kXStride = kXCols + 4;                          // floats per staged row (+pad)
 constexpr int kOffX = kOffQS + kQSBytes;                      // epilogue staging 128 rows
 constexpr int kXBytes = 128 * kXStride * 4;
 constexpr int kOffML = kOffX + kXBytes;           // (m, l) of the 128 M-rows, 2 buffers
-constexpr int kOffBar = kOffML + 2 * 128 * 8;
-constexpr int kItemRing = 8;                      // claimed-item broadcast ring
+constexpr int kItemRing = 8;                      // claimed-item ring (ItemRec, 512 B each)
+constexpr int kOffRec = kOffML + 2 * 128 * 8;
+constexpr int kOffBar = kOffRec + kItemRing * 512;
 constexpr int kSmemUsed = kOffBar + 512;
 constexpr int kSmemBytes = kSmemUsed + 1024;      // + alignment slack
-// warp 0: item claimer + K producer; warp 1: MMA issuer; warps 2-5: softmax;
-// warps 6-9: epilogue; warp 10: V producer
-constexpr int kAttnThreads = 352;
+// warp 0: K producer; warp 1: MMA issuer; warps 2-5: softmax; warps 6-9: epilogue;
+// warp 10: V producer; warp 11: item scheduler (claims, resolves tiles, stages queries)
+constexpr int kAttnThreads = 384;
+constexpr int kRingConsumers = 11;  // warps 0-10 release every item record
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0;     // S0 / P0 [0, 64), S1 / P1 [64, 128)
 constexpr uint32_t kColO = 128;   // O0 [128, 256), O1 [256, 384)
-constexpr uint32_t kColQ = 384;   // Q [384, 448): 128 bf16 per row as 64 packed columns
+constexpr uint32_t kColQ = 384;   // Q0 [384, 448), Q1 [448, 512): 128 bf16 per row, 64 packed cols
 
 constexpr uint32_t kIdescQK = umma_idesc_bf16(128, 64, false, false);
 constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, false, true);
@@ -100,16 +103,25 @@ __device__ __forceinline__ int mrow_of(int m64, int wq, int lane) {
   return lane < 16 ? wq * 16 + lane : -1;
 }
 
-__device__ __forceinline__ void decode_item(const AttnParams &p, int it, Item &x) {
-  const int q = it / p.h_local;
-  x.g = it - q * p.h_local;
-  const int4 a = __ldg(reinterpret_cast<const int4 *>(p.items + q));
-  const int4 b = __ldg(reinterpret_cast<const int4 *>(p.items + q) + 1);
-  x.r = a.x; x.w = a.y; x.adm_off = a.z; x.cs0 = a.w;
-  x.tb = b.x; x.te = b.y; x.nt = b.z;
-  x.local = b.w & 1;
-  x.rep = (b.w >> 1) & 7;
-  x.m64 = (b.w >> 4) & 1;
+// A claimed work item as the scheduler warp resolves it into SMEM: the descriptor plus, per
+// 64-token tile, its first token, valid tokens, owning branch (-1: all rows) and the page of
+// each 16-token box.  Every other role reads only this record (no global loads per item).
+struct ItemRec {
+  int32_t it, g, desc[8];  // desc = ItemDesc {r, w, adm_off, cs0, tb, te, nt, flags}
+  int32_t pad[6];
+  int32_t tok0[kLocalItemTiles], valid[kLocalItemTiles], jrow[kLocalItemTiles];
+  int32_t pg[kLocalItemTiles][4];
+};
+static_assert(sizeof(ItemRec) == 512, "ItemRec size");
+
+__device__ __forceinline__ void decode_item(const ItemRec *rec, Item &x) {
+  x.g = rec->g;
+  x.r = rec->desc[0]; x.w = rec->desc[1]; x.adm_off = rec->desc[2]; x.cs0 = rec->desc[3];
+  x.tb = rec->desc[4]; x.te = rec->desc[5]; x.nt = rec->desc[6];
+  const int f = rec->desc[7];
+  x.local = f & 1;
+  x.rep = (f >> 1) & 7;
+  x.m64 = (f >> 4) & 1;
 }
 
 struct TileInfo {
@@ -134,11 +146,9 @@ __device__ __forceinline__ TileInfo tile_info(const AttnParams &p, const Item &x
   return ti;
 }
 
-// valid tokens and owning branch of tile t (softmax side: no page lookup)
-__device__ __forceinline__ int2 tile_rows(const AttnParams &p, const Item &x, int t) {
-  if (!x.local) return make_int2(min(kTile, x.te - (x.tb + t * kTile)), -1);
-  const int4 lt = __ldg(p.ltiles + x.tb + t);
-  return make_int2(lt.z, lt.w);
+// valid tokens and owning branch of tile t (softmax side)
+__device__ __forceinline__ int2 tile_rows(const ItemRec *rec, int t) {
+  return make_int2(rec->valid[t], rec->jrow[t]);
 }
 
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
@@ -150,12 +160,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 
 // Move the item's staged stacked queries (SMEM, [row][128] bf16, filled by the producer's
-// bulk copies in passes of 64 rows) into TMEM columns [kColQ, kColQ+64), replicated over
+// bulk copies in passes of 64 rows) into TMEM columns [qcol, qcol + 64), replicated over
 // the row copies; each pass's buffer is released after use.  Ends with the tcgen05 stores
 // complete and fenced.  `pass` counts staging passes consumed so far (updated).
 __device__ __forceinline__ void stage_q_tmem(const Item &x, const uint8_t *qs, uint64_t *qs_full,
                                              uint64_t *qs_free, uint32_t &pass, uint32_t tmem,
-                                             uint32_t lane_off, int wq, int lane) {
+                                             uint32_t lane_off, int wq, int lane, uint32_t qcol) {
   const int R8 = 8 * x.w;
   const int m = mrow_of(x.m64, wq, lane);
   const int rpc = (x.m64 ? 64 : 128) / x.rep;
@@ -166,7 +176,7 @@ __device__ __forceinline__ void stage_q_tmem(const Item &x, const uint8_t *qs, u
   for (int r0 = 0; r0 < R8; r0 += kQSRows, ++pass) {
     mbar_wait(qs_full, pass & 1);
     if (i >= r0 && i < min(R8, r0 + kQSRows)) {
-      const uint4 *src = reinterpret_cast<const uint4 *>(qs + (i - r0) * 256);
+      const uint4 *src = reinterpret_cast<const uint4 *>(qs + (i - r0) * kQSStride);
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         const uint4 u = src[c];
@@ -175,7 +185,7 @@ __device__ __forceinline__ void stage_q_tmem(const Item &x, const uint8_t *qs, u
     }
     mbar_arrive(qs_free);
   }
-  tmem_st_n<64>(tmem + lane_off + kColQ, v);
+  tmem_st_n<64>(tmem + lane_off + qcol, v);
   tmem_st_wait();
   tc_fence_before();
 }
@@ -320,10 +330,10 @@ __device__ __forceinline__ void softmax_tile(uint32_t tS, int colbase, int nvali
 }
 
 // Consumer side of the claimed-item ring: the k-th item this CTA processes (-1 = done).
-__device__ __forceinline__ int ring_item(uint64_t *it_full, const int32_t *it_ring, uint32_t k) {
+__device__ __forceinline__ int ring_item(uint64_t *it_full, const ItemRec *recs, uint32_t k) {
   const uint32_t slot = k % kItemRing;
   mbar_wait(it_full + slot, (k / kItemRing) & 1);
-  return *reinterpret_cast<const volatile int32_t *>(it_ring + slot);
+  return *reinterpret_cast<const volatile int32_t *>(&recs[slot].it);
 }
 __device__ __forceinline__ void ring_release(uint64_t *it_empty, uint32_t k, int lane) {
   __syncwarp();
@@ -351,10 +361,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t *ml_full = o_free + 2;          // [2] softmax (m, l) published -> epilogue
   uint64_t *qs_full = ml_full + 2;         // producer's Q staging copy landed
   uint64_t *qs_free = qs_full + 1;         // softmax moved the staged Q into TMEM
-  uint64_t *it_full = qs_free + 1;         // [kItemRing] producer claimed an item
-  uint64_t *it_empty = it_full + kItemRing;  // [kItemRing] 9 consumer warps read it
-  int32_t *it_ring = reinterpret_cast<int32_t *>(it_empty + kItemRing);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(it_ring + kItemRing);
+  uint64_t *it_full = qs_free + 1;         // [kItemRing] scheduler published an item record
+  uint64_t *it_empty = it_full + kItemRing;  // [kItemRing] all consumer warps are done with it
+  uint64_t *sched_go = it_empty + kItemRing;  // K producer started an item -> scheduler
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sched_go + 1);
+  ItemRec *recs = reinterpret_cast<ItemRec *>(smem + kOffRec);
   float *xo = reinterpret_cast<float *>(smem + kOffX);
   float2 *xml = reinterpret_cast<float2 *>(smem + kOffML);
 
@@ -386,7 +397,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     mbar_init(q_full, 128);
     mbar_init(qs_full, 1);
     mbar_init(qs_free, 128);
-    for (int i = 0; i < kItemRing; ++i) { mbar_init(it_full + i, 1); mbar_init(it_empty + i, 10); }
+    for (int i = 0; i < kItemRing; ++i) {
+      mbar_init(it_full + i, 1);
+      mbar_init(it_empty + i, kRingConsumers);
+    }
+    mbar_init(sched_go, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -396,11 +411,78 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 || warp == 10) {
-    // ======================= TMA producers: warp 0 = K (+ item claimer), warp 10 = V ====
-    // At each item start lane l resolves tile l's geometry and page indices (parallel
-    // loads); the tile loop then only shuffles them to the elected issuing lane, with
-    // warp-uniform operands (no per-instruction waterfall loops).
+  if (warp == 11) {
+    // ======================= item scheduler ==================================================
+    // Claims work items (global atomic counter -> dynamic scheduling) one item ahead of the
+    // K producer, resolves each into an SMEM ItemRec (descriptor, tile geometry, page
+    // indices: lane l resolves tile l), publishes it, then stages the item's stacked queries
+    // (w slots x 8 heads x 256 B, 2 KB per slot) into SMEM by bulk copies in passes of 8
+    // slots for the softmax warps.  The dependent global loads of an item thus overlap the
+    // previous item instead of stalling the pipeline at every item boundary.
+    const int box_tok = p.page_size < kTile ? p.page_size : kTile;
+    const int n_items = (__ldg(p.hdr) + __ldg(p.hdr + 5)) * p.h_local;
+    int *work_counter = const_cast<int *>(p.hdr) + 8;
+    uint32_t qs_pass = 0;
+    for (uint32_t k = 0;; ++k) {
+      if (k >= 1) mbar_wait(sched_go, (k - 1) & 1);  // K producer started item k-1
+      int it = 0;
+      if (lane == 0) it = atomicAdd(work_counter, 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= n_items) it = -1;
+      const uint32_t slot = k % kItemRing;
+      ItemRec *rec = recs + slot;
+      mbar_wait(it_empty + slot, ((k / kItemRing) & 1) ^ 1);
+      int w = 0, adm_off = 0, g = 0;
+      if (it >= 0) {
+        const int q = it / p.h_local;
+        g = it - q * p.h_local;
+        const int32_t d = lane < 8 ? __ldg(reinterpret_cast<const int32_t *>(p.items + q) + lane) : 0;
+        const int nt = __shfl_sync(0xffffffffu, d, 6);
+        Item x;
+        x.r = __shfl_sync(0xffffffffu, d, 0);
+        w = __shfl_sync(0xffffffffu, d, 1);
+        adm_off = __shfl_sync(0xffffffffu, d, 2);
+        x.tb = __shfl_sync(0xffffffffu, d, 4);
+        x.te = __shfl_sync(0xffffffffu, d, 5);
+        x.local = __shfl_sync(0xffffffffu, d, 7) & 1;
+        if (lane < 8) rec->desc[lane] = d;
+        if (lane < nt) {
+          const TileInfo ti = tile_info(p, x, lane);
+          rec->tok0[lane] = ti.tok0;
+          rec->valid[lane] = ti.valid;
+          rec->jrow[lane] = ti.jrow;
+#pragma unroll
+          for (int b = 0; b < kTile / 16; ++b)
+            rec->pg[lane][b] =
+                b * box_tok < ti.valid ? __ldg(ti.pages + (ti.tok0 + b * box_tok) / p.page_size) : 0;
+        }
+      }
+      if (lane == 0) { rec->it = it; rec->g = g; }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(it_full + slot);  // release: the record is visible
+      if (it < 0) break;
+      const int slot_j = lane < w ? __ldg(p.adm_by_req + adm_off + lane) : 0;
+      for (int j0 = 0; j0 < w; j0 += kQSRows / 8, ++qs_pass) {
+        const int nj = min(kQSRows / 8, w - j0);
+        mbar_wait(qs_free, (qs_pass & 1) ^ 1);
+        if (elect_one()) mbar_arrive_expect_tx(qs_full, nj * 2048);
+        __syncwarp();
+        // one 256 B copy per stacked row (slot j, head e) into the padded staging rows
+        for (int rr = lane; rr < kQSRows; rr += 32) {
+          const int j = rr >> 3;
+          const int s_j = __shfl_sync(0xffffffffu, slot_j, min(j0 + j, 31));
+          if (j < nj)
+            bulk_g2s(smem + kOffQS + rr * kQSStride,
+                     p.q + ((size_t)s_j * (kGroup * p.h_local) + g * kGroup + (rr & 7)) * kHeadDim,
+                     256, qs_full);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 0 || warp == 10) {
+    // ======================= TMA producers: warp 0 = K, warp 10 = V =======================
+    // Tile geometry and pages come from the item record in SMEM; the whole warp runs the
+    // loop with warp-uniform operands and one elected lane issues (no waterfall loops).
     const bool is_k = warp == 0;
     const CUtensorMap *tmap = is_k ? &tmK : &tmV;
     uint64_t *ring_full = is_k ? kfull : vfull;
@@ -410,68 +492,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int box_tok = p.page_size < kTile ? p.page_size : kTile;
     const uint32_t half_box_bytes = box_tok * 128;
     uint32_t n_prod = 0;  // global tile counter
-    uint32_t qs_pass = 0;  // query staging passes issued
-    int *work_counter = const_cast<int *>(p.hdr) + 8;
     for (uint32_t k = 0;; ++k) {
-      int it;
-      if (is_k) {
-        // claim the next item (dynamic scheduling) and broadcast it to the other roles
-        it = 0;
-        if (lane == 0) it = atomicAdd(work_counter, 1);
-        it = __shfl_sync(0xffffffffu, it, 0);
-        if (it >= n_items) it = -1;
-        const uint32_t slot = k % kItemRing;
-        mbar_wait(it_empty + slot, ((k / kItemRing) & 1) ^ 1);
-        if (lane == 0) {
-          *reinterpret_cast<volatile int32_t *>(it_ring + slot) = it;
-          mbar_arrive(it_full + slot);
-        }
-        // the claimer also consumes its own slot
-        __syncwarp();
-        if (lane == 0) mbar_arrive(it_empty + slot);
-      } else {
-        it = ring_item(it_full, it_ring, k);
+      const int it = ring_item(it_full, recs, k);
+      if (it < 0) {
         ring_release(it_empty, k, lane);
+        break;
       }
-      if (it < 0) break;
-      Item x;
-      decode_item(p, it, x);
+      const ItemRec *rec = recs + (k % kItemRing);
       if (is_k) {
-        // stage the item's stacked queries (w slots x 8 heads x 256 B, 2 KB per slot) in SMEM
-        // by bulk copies (passes of 8 slots), so the softmax warps find them there
-        const int w_u = __shfl_sync(0xffffffffu, x.w, 0);
-        const int slot_j = lane < w_u ? __ldg(p.adm_by_req + x.adm_off + lane) : 0;
-        for (int j0 = 0; j0 < w_u; j0 += kQSRows / 8, ++qs_pass) {
-          const int nj = min(kQSRows / 8, w_u - j0);
-          mbar_wait(qs_free, (qs_pass & 1) ^ 1);
-          if (elect_one()) mbar_arrive_expect_tx(qs_full, nj * 2048);
-          __syncwarp();
-          for (int j = 0; j < nj; ++j) {
-            const int s_j = __shfl_sync(0xffffffffu, slot_j, j0 + j);
-            const __nv_bfloat16 *src =
-                p.q + ((size_t)s_j * (kGroup * p.h_local) + x.g * kGroup) * kHeadDim;
-            if (elect_one()) bulk_g2s(smem + kOffQS + j * 2048, src, 2048, qs_full);
-            __syncwarp();
-          }
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sched_go);  // the scheduler may claim the next item
       }
-      int my_tok0 = 0, my_valid = 0, my_pg[kTile / 16] = {0, 0, 0, 0};
-      if (lane < x.nt) {
-        const TileInfo ti = tile_info(p, x, lane);
-        my_tok0 = ti.tok0;
-        my_valid = ti.valid;
-#pragma unroll
-        for (int b = 0; b < kTile / 16; ++b)
-          if (b * box_tok < ti.valid) my_pg[b] = __ldg(ti.pages + (ti.tok0 + b * box_tok) / p.page_size);
-      }
-      const int g_u = __shfl_sync(0xffffffffu, x.g, 0);  // warp-uniform operands
-      const int nt_u = __shfl_sync(0xffffffffu, x.nt, 0);
+      const int g_u = rec->g;
+      const int nt_u = rec->desc[6];
       for (int t = 0; t < nt_u; ++t, ++n_prod) {
-        const int tok0 = __shfl_sync(0xffffffffu, my_tok0, t);
-        const int valid = __shfl_sync(0xffffffffu, my_valid, t);
+        const int tok0 = rec->tok0[t];
+        const int valid = rec->valid[t];
         int pg[kTile / 16];
 #pragma unroll
-        for (int b = 0; b < kTile / 16; ++b) pg[b] = __shfl_sync(0xffffffffu, my_pg[b], t);
+        for (int b = 0; b < kTile / 16; ++b) pg[b] = rec->pg[t][b];
         const uint32_t st = n_prod % n_stages;
         const int n_box = (valid + box_tok - 1) / box_tok;
         uint8_t *dst = ring + st * kStageBytes;
@@ -503,6 +542,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         __syncwarp();
         if (is_k && lane == 0) trace_ev(p, 12, n_prod);
       }
+      ring_release(it_empty, k, lane);
     }
   } else if (warp == 1) {
     // ======================= MMA issuer (whole warp, one elected lane issues) =========
@@ -512,11 +552,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
     uint32_t n = 0;  // global tile counter (S/P double buffer index = n & 1)
     for (uint32_t item_idx = 0;; ++item_idx) {
-      const int it = ring_item(it_full, it_ring, item_idx);
+      const int it = ring_item(it_full, recs, item_idx);
+      Item x;
+      decode_item(recs + item_idx % kItemRing, x);
       ring_release(it_empty, item_idx, lane);
       if (it < 0) break;
-      Item x;
-      decode_item(p, it, x);
       const int rep = __shfl_sync(0xffffffffu, x.rep, 0);
       const int m64 = __shfl_sync(0xffffffffu, x.m64, 0);
       const uint32_t idesc_qk = m64 ? kIdescQK64 : kIdescQK;
@@ -533,7 +573,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           if (lane == 0) trace_ev(p, 1, n);
           tc_fence_after();
           if (elect_one()) {
-            issue_qk(tmem_u + kColS + (n & 1) * 64, tmem_u + kColQ, sK + ks * kStageBytes, idesc_qk);
+            issue_qk(tmem_u + kColS + (n & 1) * 64, tmem_u + kColQ + (item_idx & 1) * 64,
+                     sK + ks * kStageBytes, idesc_qk);
             tc_commit(kempty + ks);
             tc_commit(s_full + (n & 1));
           }
@@ -574,16 +615,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const float c_log2 = p.scale_log2;
     uint32_t qs_pass = 0;
     uint32_t n = 0;
-    int it = ring_item(it_full, it_ring, 0);
+    int it = ring_item(it_full, recs, 0);
     if (it >= 0) {
       Item x0;
-      decode_item(p, it, x0);
-      stage_q_tmem(x0, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, wq, lane);
+      decode_item(recs, x0);
+      stage_q_tmem(x0, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, wq, lane, kColQ);
       mbar_arrive(q_full);
     }
     for (uint32_t item_idx = 0; it >= 0; ++item_idx) {
+      const ItemRec *rec = recs + item_idx % kItemRing;
       Item x;
-      decode_item(p, it, x);
+      decode_item(rec, x);
       const int R8 = 8 * x.w;
       const int rep = x.rep;
       // M-row of this thread; M = 64 rows are shared by lane pairs (t, t + 16), half h
@@ -599,9 +641,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t ob = item_idx & 1;
       const uint32_t tO = tmem + lane_off + kColO + ob * 128;
       float m_run = -INFINITY, l_run = 0.f;
+      bool staged = false;  // next item's Q staged in TMEM (or there is no next item)
+      int next = -1;
       for (int t = 0; t < x.nt; ++t) {
         const uint32_t sb = n & 1;
-        const int2 tr = tile_rows(p, x, t);  // {valid tokens, owning branch or -1}
+        const int2 tr = tile_rows(rec, t);  // {valid tokens, owning branch or -1}
         const bool live = i < R8 && (tr.y < 0 || (i >> 3) == tr.y);
         const int nvalid = live ? max(0, min(tw, tr.x - tok0)) : 0;
         mbar_wait(s_full + sb, (n >> 1) & 1);
@@ -631,17 +675,44 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         if (lane == 0) trace_ev(p, warp == 2 ? 8 : 6 + warp, n);  // warps 3,4,5 -> 9,10,11
         mbar_arrive(p_full + sb);
         ++n;
+        // Stage the next item's queries into the other Q buffer as soon as the item is
+        // claimed and its rows have landed in SMEM (never blocks here).  Q[(k+1) & 1] was
+        // last read by item k-1's QK MMAs, complete since this item's first s_full.
+        if (!staged) {
+          const uint32_t slot = (item_idx + 1) % kItemRing;
+          int ready = lane == 0 ? mbar_try_wait(it_full + slot, ((item_idx + 1) / kItemRing) & 1) : 0;
+          ready = __shfl_sync(0xffffffffu, ready, 0);
+          if (ready) {
+            next = ring_item(it_full, recs, item_idx + 1);
+            if (next < 0) {
+              staged = true;
+            } else {
+              int qready = lane == 0 ? mbar_try_wait(qs_full, qs_pass & 1) : 0;
+              qready = __shfl_sync(0xffffffffu, qready, 0);
+              if (qready) {
+                Item xn;
+                decode_item(recs + (item_idx + 1) % kItemRing, xn);
+                stage_q_tmem(xn, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, wq,
+                             lane, kColQ + ((item_idx + 1) & 1) * 64);
+                mbar_arrive(q_full);
+                staged = true;
+              }
+            }
+          }
+        }
       }
       if (m64) l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);  // row sum of the lane pair
-      // all QK MMAs of this item are complete -> stage the next item's queries
-      const int next = ring_item(it_full, it_ring, item_idx + 1);
-      ring_release(it_empty, item_idx, lane);
-      if (next >= 0) {
-        Item xn;
-        decode_item(p, next, xn);
-        stage_q_tmem(xn, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, wq, lane);
-        mbar_arrive(q_full);
+      if (!staged) {  // not staged during the item: wait for it now
+        next = ring_item(it_full, recs, item_idx + 1);
+        if (next >= 0) {
+          Item xn;
+          decode_item(recs + (item_idx + 1) % kItemRing, xn);
+          stage_q_tmem(xn, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, wq, lane,
+                       kColQ + ((item_idx + 1) & 1) * 64);
+          mbar_arrive(q_full);
+        }
       }
+      ring_release(it_empty, item_idx, lane);
       // publish (m, l) for the epilogue warps; xml[ob] was consumed by epilogue item_idx-2
       mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);
       if (h == 0) xml[ob * 128 + mrow] = make_float2(m_run, l_run);
@@ -655,11 +726,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int wq = warp & 3;
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
     for (uint32_t item_idx = 0;; ++item_idx) {
-      const int it = ring_item(it_full, it_ring, item_idx);
+      const int it = ring_item(it_full, recs, item_idx);
+      Item x;
+      decode_item(recs + item_idx % kItemRing, x);
       ring_release(it_empty, item_idx, lane);
       if (it < 0) break;
-      Item x;
-      decode_item(p, it, x);
       const int R8 = 8 * x.w;
       const int rep = x.rep;
       const int mrow = mrow_of(x.m64, wq, lane);
