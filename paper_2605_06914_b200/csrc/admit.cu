@@ -34,6 +34,9 @@ struct AdmitParams {
   int32_t *status;
   int32_t *hdr, *slot_req, *slot_rank, *req_chunk_off, *req_loc_off, *req_part_off,
       *req_adm_off, *adm_by_req;
+  int4 *merge_desc;  // [S] per admitted slot k (adm_list order): {slot, first partial
+                     //     chunk-slot, partials, admitted width of its request}
+  int32_t *done;     // [2 * R * 8] attend -> merge completion counters (zeroed here)
   int64_t cap_cs;
   int h_local;
   ItemDesc *items;   // [cap_cs] work items (A5)
@@ -358,7 +361,11 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     // <= 8 ready branches: M = 64 MMAs (16 rows per TMEM lane quadrant), replicated 4 / 2 / 1
     // times for <= 16 / 32 / 64 stacked rows; else M = 128 without replication
     const int m64 = (8 * nr <= 64) ? 1 : 0;
+#ifdef TAPER_EXP_REP1
+    const int rep = 1;
+#else
     const int rep = m64 ? ((8 * nr <= 16) ? 4 : ((8 * nr <= 32) ? 2 : 1)) : 1;
+#endif
     const int nc = p.req_chunk_off[r + 1] - p.req_chunk_off[r];
     const int cs_r = p.req_part_off[r];
     for (int c = 0; c < nc; ++c) {
@@ -367,7 +374,11 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       d.tb = c * kChunk; d.te = min(d.tb + kChunk, p.Lsh[r]);
       d.nt = (d.te - d.tb + kTileTokens - 1) / kTileTokens;
       d.flags = (rep << 1) | (m64 << 4);
+#ifdef TAPER_CHUNKS_FIRST
+      p.items[p.req_chunk_off[r] + c] = d;
+#else
       p.items[p.req_chunk_off[r] + p.req_loc_off[r] + c] = d;  // request-major numbering
+#endif
     }
     // local tiles of the admitted branches, branch-major, grouped 16 per local item
     const int l0 = p.req_loc_off[r], nl = p.req_loc_off[r + 1] - l0;
@@ -385,9 +396,14 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       d.tb = (l0 + li) * kLocalItemTiles; d.te = 0;
       d.nt = min(kLocalItemTiles, lt - li * kLocalItemTiles);
       d.flags = 1 | (rep << 1) | (m64 << 4);
+#ifdef TAPER_CHUNKS_FIRST
+      p.items[p.req_chunk_off[R] + l0 + li] = d;
+#else
       p.items[p.req_chunk_off[r] + l0 + nc + li] = d;
+#endif
     }
   }
+  for (int i = tid; i < 2 * R * kGroup; i += blockDim.x) p.done[i] = 0;
   // adm_list: ascending slot index
   int f[kPerThread];
 #pragma unroll
@@ -402,7 +418,14 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
 #pragma unroll
   for (int k = 0; k < kPerThread; ++k) {
     int s = tid * kPerThread + k;
-    if (s < S && f[k]) p.adm_list[fl[k]] = s;
+    if (s < S && f[k]) {
+      p.adm_list[fl[k]] = s;
+      const int r = p.slot_req[s];
+      const int nq = (p.req_chunk_off[r + 1] - p.req_chunk_off[r]) +
+                     (p.req_loc_off[r + 1] - p.req_loc_off[r]);
+      p.merge_desc[fl[k]] = make_int4(s, p.req_part_off[r] + p.slot_rank[s], nq,
+                                      (p.req_adm_off[r + 1] - p.req_adm_off[r]) | (r << 16));
+    }
   }
   if (tid == 0) {
     int st = sh_status;
@@ -416,6 +439,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     p.hdr[3] = int(p.cap_cs > 0x7fffffff ? 0x7fffffff : p.cap_cs);
     p.hdr[4] = p.h_local;
     p.hdr[8] = 0;  // dynamic work counter of the next attend_kernel
+    p.hdr[9] = 0;  // attend CTAs exited
     *p.n_adm = n_adm;
     if (p.decide) *p.status = st;
     else atomicOr(p.status, st);
@@ -474,6 +498,8 @@ static int launch_admit(const taper_batch *batch, const taper_latency_model *mod
   p.req_loc_off = reinterpret_cast<int32_t *>(w + L.req_loc_off);
   p.req_adm_off = reinterpret_cast<int32_t *>(w + L.req_adm_off);
   p.adm_by_req = reinterpret_cast<int32_t *>(w + L.adm_by_req);
+  p.merge_desc = reinterpret_cast<int4 *>(w + L.merge_desc);
+  p.done = reinterpret_cast<int32_t *>(w + L.done);
   WsTables T = ws_tables(ws_bytes, R, S, h_local);
   p.cap_cs = T.cap_cs;
   p.items = reinterpret_cast<ItemDesc *>(w + T.items);

@@ -73,7 +73,9 @@ constexpr uint32_t kIdescPV64 = umma_idesc_bf16(64, 128, false, true);
 
 struct AttnParams {
   const int32_t *slot_page_off, *slot_pages, *req_page_off, *req_pages;
-  const int32_t *hdr, *adm_by_req;
+  int32_t *hdr;        // hdr[8]: work counter, hdr[9]: CTAs exited
+  const int32_t *adm_by_req;
+  int32_t *done;       // [r * 8 + g]: items of (request, KV head) whose partials are written
   const ItemDesc *items;
   const int4 *ltiles;
   const __nv_bfloat16 *q;
@@ -224,7 +226,11 @@ __device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t vb, 
     uint32_t mask[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) mask[q] = (REP == 1 || q / (4 / REP) == c) ? 0u : 0xffffffffu;
+#ifdef TAPER_EXP_NO_LO
+    constexpr int kParts = 1;  // power experiment only: drops the lo part (wrong numerics)
+#else
     constexpr int kParts = 2;  // P = hi + lo
+#endif
 #pragma unroll
     for (int part = 0; part < kParts; ++part) {
 #pragma unroll
@@ -410,6 +416,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: the prologue above overlapped the previous kernel; the merge kernel may launch now
+  // (it waits for per-request completion counters); wait for the previous kernel's memory.
+  pdl_launch_dependents();
+  pdl_wait();
 
   if (warp == 11) {
     // ======================= item scheduler ==================================================
@@ -421,7 +431,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // previous item instead of stalling the pipeline at every item boundary.
     const int box_tok = p.page_size < kTile ? p.page_size : kTile;
     const int n_items = (__ldg(p.hdr) + __ldg(p.hdr + 5)) * p.h_local;
-    int *work_counter = const_cast<int *>(p.hdr) + 8;
+    int *work_counter = p.hdr + 8;
     uint32_t qs_pass = 0;
     for (uint32_t k = 0;; ++k) {
       if (k >= 1) mbar_wait(sched_go, (k - 1) & 1);  // K producer started item k-1
@@ -793,6 +803,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
         named_bar_sync(2, 128);  // staging reused by the next pass / item
       }
+      // publish: this item's partials of (request, KV head) are complete (release)
+      __threadfence();
+      named_bar_sync(2, 128);
+      if (etid == 0) atomicAdd(p.done + x.r * kGroup + x.g, 1);
       if (warp == 6 && lane == 0) trace_ev(p, 14, 2048 + item_idx);
       if (warp == 8 && lane == 0) trace_ev(p, 15, 2048 + item_idx);
       tc_fence_before();
@@ -806,6 +820,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
   }
+  if (tid == 0) {
+    // the last CTA to exit re-arms the work counter for the next launch (all claims are done)
+    __threadfence();
+    if (atomicAdd(p.hdr + 9, 1) == int(gridDim.x) - 1) {
+      __threadfence();
+      p.hdr[8] = 0;
+      p.hdr[9] = 0;
+    }
+  }
   if (p.trace != nullptr && tid == 0) {
     unsigned long long g;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
@@ -814,70 +837,113 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 }
 
 // ------------------------------------------------------------------ A8: LSE merge
-constexpr int kMergeThreads = 256;  // one warp per (admitted slot, KV head)
+constexpr int kMergeThreads = 256;  // one CTA per admitted slot, one warp per KV head
 
 struct MergeParams {
-  const int32_t *hdr, *slot_req, *slot_rank, *req_chunk_off, *req_loc_off, *req_part_off,
-      *req_adm_off, *adm_list;
+  long long *trace;  // debug: per-CTA globaltimer span at rows 3200 + CTA (taper_set_trace_buffer)
+  int trace_cap;
+  const int32_t *hdr;
+  const int4 *merge_desc;
+  int32_t *done;  // [R * 8] completion counters (attend), [R * 8, 2 R * 8) readers done
+  int R;
   const float *part_lse, *part_o;
   __nv_bfloat16 *out;
   float *lse_out;
   int h_local;
 };
 
-__global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
-  const int lane = threadIdx.x & 31;
-  // the attend kernel of this call has finished (stream order): re-arm its work counter
-  if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<int32_t *>(p.hdr)[8] = 0;
+// Per (admitted slot, KV head): the slot's partials are 8 contiguous GQA rows (4 KB) per
+// work item, so the warp streams whole 4 KB blocks (lane: dims 4 lane .. 4 lane + 3 of all 8
+// rows) and runs the 8 rows' online LSE merges side by side, partials in work order
+// (prefix chunks, then local items), two items' loads in flight at a time.
+// Launched with PDL while attend_kernel is still running: a warp starts as soon as the
+// attend epilogues have published all items of its (request, KV head) (acquire on the
+// completion counter), so the merge overlaps the attend kernel's tail.
+__global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool tr = p.trace != nullptr && threadIdx.x == 0 && 3200 + int(blockIdx.x) < p.trace_cap;
+  if (tr) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    p.trace[(size_t)(3200 + blockIdx.x) * 16 + 0] = (long long)g;
+  }
+  pdl_launch_dependents();
   const int h = p.h_local;
-  const int n_rows = __ldg(p.hdr + 2) * h * kGroup;  // (admitted slot, KV head, GQA row)
+  const int n_adm = __ldg(p.hdr + 2);
   const int qheads = kGroup * h;
-  const int warps = gridDim.x * (kMergeThreads / 32);
-  // one warp per output row: lane owns 4 of the 128 dims; single-pass online LSE merge of
-  // the row's partials (prefix chunks in order, then local items) with batched loads
-  for (int it = blockIdx.x * (kMergeThreads / 32) + (threadIdx.x >> 5); it < n_rows; it += warps) {
-    const int a = it % kGroup, kg = it / kGroup;
-    const int k = kg / h, g = kg - k * h;
-    const int s = __ldg(p.adm_list + k);
-    const int r = __ldg(p.slot_req + s);
-    const int j = __ldg(p.slot_rank + s);
-    const int w = __ldg(p.req_adm_off + r + 1) - __ldg(p.req_adm_off + r);
-    const int nq = (__ldg(p.req_chunk_off + r + 1) - __ldg(p.req_chunk_off + r)) +
-                   (__ldg(p.req_loc_off + r + 1) - __ldg(p.req_loc_off + r));
-    const size_t row0 = ((size_t)(__ldg(p.req_part_off + r) + j) * h + g) * kGroup + a;
-    const size_t qstride = (size_t)w * h * kGroup;  // partial rows between items of r
-    float M = -INFINITY, Z = 0.f;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int q0 = 0; q0 < nq; q0 += 4) {
-      float l2[4];
-      float4 v[4];
+  for (int k = blockIdx.x; k < n_adm; k += gridDim.x) {
+    const int4 md = __ldg(p.merge_desc + k);  // {slot, first chunk-slot, partials, width | r << 16}
+    const int s = md.x, nq = md.z, w = md.w & 0xffff, r = md.w >> 16;
+    for (int g = warp; g < h; g += kMergeThreads / 32) {
+      const size_t row0 = ((size_t)md.y * h + g) * kGroup;
+      const size_t qstride = (size_t)w * h * kGroup;  // partial rows between items
+      int32_t *cnt = p.done + r * kGroup + g;
+      if (ld_acquire(cnt) < nq) {  // bounded spin: a lost publication traps, never hangs
+        const long long t0 = clock64();
+        while (ld_acquire(cnt) < nq) {
+          __nanosleep(256);
+          if (clock64() - t0 > (1ll << 35)) __trap();
+        }
+      }
+      float M[kGroup], Z[kGroup];
+      float4 acc[kGroup];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const bool ok = q0 + u < nq;
-        const size_t prow = row0 + (size_t)(q0 + u) * qstride;
-        l2[u] = ok ? __ldg(p.part_lse + prow) * 1.4426950408889634f : -INFINITY;
-        v[u] = ok ? __ldg(reinterpret_cast<const float4 *>(p.part_o + prow * kHeadDim) + lane)
-                  : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int a = 0; a < kGroup; ++a) {
+        M[a] = -INFINITY; Z[a] = 0.f; acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      for (int q0 = 0; q0 < nq; q0 += 2) {
+        float4 v[2][kGroup];
+        float l2 = -INFINITY;  // lane u * 8 + a: lse of row a of item q0 + u (log2 units)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const bool ok = q0 + u < nq;
+          const size_t prow = row0 + (size_t)(q0 + u) * qstride;
+          if (ok && (lane >> 3) == u) l2 = __ldcg(p.part_lse + prow + (lane & 7)) * 1.4426950408889634f;
+#pragma unroll
+          for (int a = 0; a < kGroup; ++a)
+            v[u][a] = ok ? __ldcg(reinterpret_cast<const float4 *>(p.part_o + (prow + a) * kHeadDim) + lane)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+#pragma unroll
+          for (int a = 0; a < kGroup; ++a) {
+            const float lq = __shfl_sync(0xffffffffu, l2, u * 8 + a);
+            if (lq == -INFINITY) continue;
+            const float Mn = fmaxf(M[a], lq);
+            const float sc = ex2(M[a] - Mn), wgt = ex2(lq - Mn);  // ex2(-inf) = 0
+            acc[a].x = acc[a].x * sc + wgt * v[u][a].x; acc[a].y = acc[a].y * sc + wgt * v[u][a].y;
+            acc[a].z = acc[a].z * sc + wgt * v[u][a].z; acc[a].w = acc[a].w * sc + wgt * v[u][a].w;
+            Z[a] = Z[a] * sc + wgt;
+            M[a] = Mn;
+          }
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (l2[u] == -INFINITY) continue;
-        const float Mn = fmaxf(M, l2[u]);
-        const float sc = ex2(M - Mn), wgt = ex2(l2[u] - Mn);  // ex2(-inf) = 0
-        acc.x = acc.x * sc + wgt * v[u].x; acc.y = acc.y * sc + wgt * v[u].y;
-        acc.z = acc.z * sc + wgt * v[u].z; acc.w = acc.w * sc + wgt * v[u].w;
-        Z = Z * sc + wgt;
-        M = Mn;
+      for (int a = 0; a < kGroup; ++a) {
+        const float inv = 1.f / Z[a];
+        __align__(8) __nv_bfloat162 o2[2];
+        o2[0] = __floats2bfloat162_rn(acc[a].x * inv, acc[a].y * inv);
+        o2[1] = __floats2bfloat162_rn(acc[a].z * inv, acc[a].w * inv);
+        *reinterpret_cast<uint2 *>(p.out + ((size_t)s * qheads + g * kGroup + a) * kHeadDim + 4 * lane) =
+            *reinterpret_cast<uint2 *>(o2);
+        if (p.lse_out && lane == a)
+          p.lse_out[(size_t)s * qheads + g * kGroup + a] = (M[a] + __log2f(Z[a])) * 0.69314718055994531f;
+      }
+      // the last of the request's w readers re-arms the counters for the next call
+      __syncwarp();
+      if (lane == 0 && atomicAdd(cnt + p.R * kGroup, 1) == w - 1) {
+        *cnt = 0;
+        cnt[p.R * kGroup] = 0;
       }
     }
-    const float inv = 1.f / Z;
-    __align__(8) __nv_bfloat162 o2[2];
-    o2[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-    o2[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
-    *reinterpret_cast<uint2 *>(p.out + ((size_t)s * qheads + g * kGroup + a) * kHeadDim + 4 * lane) =
-        *reinterpret_cast<uint2 *>(o2);
-    if (p.lse_out && lane == 0)
-      p.lse_out[(size_t)s * qheads + g * kGroup + a] = (M + __log2f(Z)) * 0.69314718055994531f;
+  }
+  pdl_wait();  // complete only after attend_kernel (its counter re-arm) has completed
+  if (tr) {
+    __syncwarp();
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    p.trace[(size_t)(3200 + blockIdx.x) * 16 + 1] = (long long)g;
   }
 }
 
@@ -1006,7 +1072,8 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   ap.slot_pages = kv->slot_pages;
   ap.req_page_off = kv->req_page_off;
   ap.req_pages = kv->req_pages;
-  ap.hdr = reinterpret_cast<const int32_t *>(w + L.hdr);
+  ap.hdr = reinterpret_cast<int32_t *>(w + L.hdr);
+  ap.done = reinterpret_cast<int32_t *>(w + L.done);
   ap.adm_by_req = reinterpret_cast<const int32_t *>(w + L.adm_by_req);
   ap.items = reinterpret_cast<const ItemDesc *>(w + tabs.items);
   ap.ltiles = reinterpret_cast<const int4 *>(w + tabs.ltiles);
@@ -1021,29 +1088,41 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   ap.trace_cap = g_trace_cap;
   const int sms = device_sms();
   if (g_prof_ev[0]) cudaEventRecord(g_prof_ev[0], st);
-  attend_kernel<<<sms, kAttnThreads, kSmemBytes, st>>>(tmK, tmV, ap);
-  cudaError_t e = cudaGetLastError();
+  // both kernels launch with programmatic stream serialization (PDL): each may start while
+  // its predecessor drains and synchronises in-kernel (griddepcontrol / completion counters)
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(kAttnThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attend_kernel, tmK, tmV, ap);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail_cuda(e, "attend_kernel launch");
   if (g_prof_ev[1]) cudaEventRecord(g_prof_ev[1], st);
 
   MergeParams mp;
+  mp.trace = g_trace;
+  mp.trace_cap = g_trace_cap;
   mp.hdr = ap.hdr;
-  mp.slot_req = reinterpret_cast<const int32_t *>(w + L.slot_req);
-  mp.slot_rank = reinterpret_cast<const int32_t *>(w + L.slot_rank);
-  mp.req_chunk_off = reinterpret_cast<const int32_t *>(w + L.req_chunk_off);
-  mp.req_loc_off = reinterpret_cast<const int32_t *>(w + L.req_loc_off);
-  mp.req_part_off = reinterpret_cast<const int32_t *>(w + L.req_part_off);
-  mp.req_adm_off = reinterpret_cast<const int32_t *>(w + L.req_adm_off);
-  mp.adm_list = adm->adm_list;
+  mp.done = ap.done;
+  mp.R = R;
+  mp.merge_desc = reinterpret_cast<const int4 *>(w + L.merge_desc);
   mp.part_lse = ap.part_lse;
   mp.part_o = ap.part_o;
   mp.out = static_cast<__nv_bfloat16 *>(out);
   mp.lse_out = lse;
   mp.h_local = h;
-  int grid = (S * h * kGroup + (kMergeThreads / 32) - 1) / (kMergeThreads / 32);
-  if (grid > sms * 8) grid = sms * 8;
-  merge_kernel<<<grid, kMergeThreads, 0, st>>>(mp);
-  e = cudaGetLastError();
+  const int grid = S > 0 ? S : 1;  // CTAs beyond the admitted count exit at once
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kMergeThreads);
+  cfg.dynamicSmemBytes = 0;
+  e = cudaLaunchKernelEx(&cfg, merge_kernel, mp);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail_cuda(e, "merge_kernel launch");
   if (g_prof_ev[2]) cudaEventRecord(g_prof_ev[2], st);
   set_launches(2);

@@ -24,10 +24,11 @@ constexpr int kLocalItemTiles = 16;   // branch-local tiles per local work item
 // hdr[3] = cap_cs  : chunk-slot capacity of the partial buffers (for this h_local)
 // hdr[4] = h_local
 // hdr[5] = n_rl    : number of (request, local item) pairs (local items per KV head)
-// hdr[8] = work counter of attend_kernel's dynamic scheduler (reset by admit and merge)
+// hdr[8] = work counter of attend_kernel's dynamic scheduler (reset by admit and by the
+//          last attend CTA to exit, counted in hdr[9])
 struct WsLayout {
   size_t hdr, slot_req, slot_rank, req_chunk_off, req_loc_off, req_part_off, req_adm_off,
-      adm_by_req, part_lse, part_o, fixed;
+      adm_by_req, merge_desc, done, part_lse, part_o, fixed;
 };
 
 __host__ __device__ inline size_t ws_align(size_t x) { return (x + 255) & ~size_t(255); }
@@ -43,6 +44,10 @@ __host__ __device__ inline WsLayout ws_layout(int R, int S) {
   w.req_part_off = o;  o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
   w.req_adm_off = o;   o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
   w.adm_by_req = o;    o = ws_align(o + size_t(S) * sizeof(int32_t));
+  w.merge_desc = o;    o = ws_align(o + size_t(S) * 4 * sizeof(int32_t));
+  // per (request, KV head): [0, R*8) items whose partials are written (attend -> merge),
+  // [R*8, 2*R*8) merge warps done reading them (the last one re-arms both)
+  w.done = o;          o = ws_align(o + size_t(R) * 2 * kGroup * sizeof(int32_t));
   w.fixed = o;
   w.part_lse = o;  // sized at run time from the workspace bytes
   w.part_o = o;
@@ -131,6 +136,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
     if (clock64() - t0 > (1ll << 35)) __trap();  // ~17 s at 2 GHz
   }
+}
+
+// Programmatic dependent launch (PDL): let the next kernel in the stream launch / wait
+// for the previous one's completion and memory.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {

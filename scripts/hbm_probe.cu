@@ -250,8 +250,9 @@ void run_tma(const uint8_t *pool, const int *order, int n_pages, int page_bytes,
          (double)n_pages * page_bytes / (ms * 1e-3) / 1e9, e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
-int main() {
+int main(int argc, char **argv) {
   setvbuf(stdout, nullptr, _IONBF, 0);
+  const int burn = argc > 1 ? atoi(argv[1]) : 0;  // >0: repeat the 2-producer tensor probe N times (power check)
   const int page_bytes = 16384;  // one (page, head) K block: 64 tokens x 128 d bf16
   const size_t pool_bytes = size_t(4) << 30;  // 4 GiB >> L2
   const int n_pages = int(pool_bytes / page_bytes);
@@ -275,6 +276,9 @@ int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   printf("SMs %d, pool %.1f GB, random 16 KB pages\n", sms, pool_bytes / 1e9);
+  for (int i = 0; i < burn; ++i)
+    run_tensor<5, 2, true>(pool, order, n_pages, sink, sms, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (burn) return 0;
   run_tma<4, 16384>(pool, order, n_pages, page_bytes, sink, sms, 1);
   run_tma<8, 16384>(pool, order, n_pages, page_bytes, sink, sms, 1);
   run_tma<12, 16384>(pool, order, n_pages, page_bytes, sink, sms, 1);
