@@ -361,11 +361,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     // <= 8 ready branches: M = 64 MMAs (16 rows per TMEM lane quadrant), replicated 4 / 2 / 1
     // times for <= 16 / 32 / 64 stacked rows; else M = 128 without replication
     const int m64 = (8 * nr <= 64) ? 1 : 0;
-#ifdef TAPER_EXP_REP1
-    const int rep = 1;
-#else
     const int rep = m64 ? ((8 * nr <= 16) ? 4 : ((8 * nr <= 32) ? 2 : 1)) : 1;
-#endif
     const int nc = p.req_chunk_off[r + 1] - p.req_chunk_off[r];
     const int cs_r = p.req_part_off[r];
     for (int c = 0; c < nc; ++c) {

@@ -226,11 +226,7 @@ __device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t vb, 
     uint32_t mask[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) mask[q] = (REP == 1 || q / (4 / REP) == c) ? 0u : 0xffffffffu;
-#ifdef TAPER_EXP_NO_LO
-    constexpr int kParts = 1;  // power experiment only: drops the lo part (wrong numerics)
-#else
     constexpr int kParts = 2;  // P = hi + lo
-#endif
 #pragma unroll
     for (int part = 0; part < kParts; ++part) {
 #pragma unroll
