@@ -370,11 +370,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       d.tb = c * kChunk; d.te = min(d.tb + kChunk, p.Lsh[r]);
       d.nt = (d.te - d.tb + kTileTokens - 1) / kTileTokens;
       d.flags = (rep << 1) | (m64 << 4);
-#ifdef TAPER_CHUNKS_FIRST
-      p.items[p.req_chunk_off[r] + c] = d;
-#else
       p.items[p.req_chunk_off[r] + p.req_loc_off[r] + c] = d;  // request-major numbering
-#endif
     }
     // local tiles of the admitted branches, branch-major, grouped 16 per local item
     const int l0 = p.req_loc_off[r], nl = p.req_loc_off[r + 1] - l0;
@@ -392,11 +388,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       d.tb = (l0 + li) * kLocalItemTiles; d.te = 0;
       d.nt = min(kLocalItemTiles, lt - li * kLocalItemTiles);
       d.flags = 1 | (rep << 1) | (m64 << 4);
-#ifdef TAPER_CHUNKS_FIRST
-      p.items[p.req_chunk_off[R] + l0 + li] = d;
-#else
       p.items[p.req_chunk_off[r] + l0 + nc + li] = d;
-#endif
     }
   }
   for (int i = tid; i < 2 * R * kGroup; i += blockDim.x) p.done[i] = 0;
