@@ -34,8 +34,9 @@ struct AdmitParams {
   int32_t *status;
   int32_t *hdr, *slot_req, *slot_rank, *req_chunk_off, *req_loc_off, *req_part_off,
       *req_adm_off, *adm_by_req;
-  int4 *merge_desc;  // [S] per admitted slot k (adm_list order): {slot, first partial
-                     //     chunk-slot, partials, admitted width of its request}
+  int4 *merge_desc;  // [2 S] per admitted slot k (adm_list order): {slot, first shared
+                     //     partial, prefix chunks, width}, {first local partial, local
+                     //     items, request, items of the request per KV head}
   int32_t *done;     // [2 * R * 8] attend -> merge completion counters (zeroed here)
   int64_t cap_cs;
   int h_local;
@@ -294,8 +295,9 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
   }
 
   // ---- work list (A5): per-request widths, item counts and CSR offsets.
-  // Shared items: ceil(Lsh / 1024) prefix chunks.  Local items: the admitted branches'
-  // local tiles (64 tokens, never mixing branches) in groups of kLocalItemTiles.
+  // Shared items: (1024-token prefix chunk, group of <= 8 admitted branches).  Local items:
+  // <= kLocalItemTiles 64-token tiles of ONE admitted branch's local KV.  Partials (8 rows
+  // per KV head each): shared (chunk c, branch j) at c * w + j, then one per local item.
   int w_loc[kPerThread], nc_loc[kPerThread], nl_loc[kPerThread], cs_loc[kPerThread];
 #pragma unroll
   for (int k = 0; k < kPerThread; ++k) {
@@ -304,15 +306,17 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     if (r < R) {
       int b = p.off[r], e = p.off[r + 1];
       if (!(sh_status & TAPER_STATUS_BAD_LENGTH)) {
-        int lt = 0;
         for (int s = b; s < e; ++s)
-          if (p.slot_admitted[s]) { w += 1; lt += (p.Lloc[s] + kTileTokens - 1) / kTileTokens; }
+          if (p.slot_admitted[s]) {
+            w += 1;
+            nl += (p.Lloc[s] + kTileTokens * kLocalItemTiles - 1) / (kTileTokens * kLocalItemTiles);
+          }
         if (w > 0 && p.Lsh[r] > 0) nc = (p.Lsh[r] + kChunk - 1) / kChunk;
-        nl = (lt + kLocalItemTiles - 1) / kLocalItemTiles;
       }
       p.req_width[r] = w;
     }
-    w_loc[k] = w; nc_loc[k] = nc; nl_loc[k] = nl; cs_loc[k] = w * (nc + nl);
+    const int groups = (w + kMaxItemBranches - 1) / kMaxItemBranches;
+    w_loc[k] = w; nc_loc[k] = nc * groups; nl_loc[k] = nl; cs_loc[k] = w * nc + nl;
   }
   int tot_w = block_exscan4<int>(w_loc, scan_i);
   int tot_nc = block_exscan4<int>(nc_loc, scan_i);
@@ -357,38 +361,43 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     const int w = p.req_adm_off[r + 1] - p.req_adm_off[r];
     if (w == 0) continue;
     const int adm_off = p.req_adm_off[r];
-    const int nr = p.off[r + 1] - p.off[r];
-    // <= 8 ready branches: M = 64 MMAs (16 rows per TMEM lane quadrant), replicated 4 / 2 / 1
-    // times for <= 16 / 32 / 64 stacked rows; else M = 128 without replication
-    const int m64 = (8 * nr <= 64) ? 1 : 0;
-    const int rep = m64 ? ((8 * nr <= 16) ? 4 : ((8 * nr <= 32) ? 2 : 1)) : 1;
-    const int nc = p.req_chunk_off[r + 1] - p.req_chunk_off[r];
+    const int nsh = p.req_chunk_off[r + 1] - p.req_chunk_off[r];  // shared items
+    const int groups = (w + kMaxItemBranches - 1) / kMaxItemBranches;
+    const int nc = nsh / groups;
     const int cs_r = p.req_part_off[r];
-    for (int c = 0; c < nc; ++c) {
-      ItemDesc d;
-      d.r = r; d.w = w; d.adm_off = adm_off; d.cs0 = cs_r + c * w;
-      d.tb = c * kChunk; d.te = min(d.tb + kChunk, p.Lsh[r]);
-      d.nt = (d.te - d.tb + kTileTokens - 1) / kTileTokens;
-      d.flags = (rep << 1) | (m64 << 4);
-      p.items[p.req_chunk_off[r] + p.req_loc_off[r] + c] = d;  // request-major numbering
-    }
-    // local tiles of the admitted branches, branch-major, grouped 16 per local item
-    const int l0 = p.req_loc_off[r], nl = p.req_loc_off[r + 1] - l0;
-    int lt = 0;
+    const int it0 = p.req_chunk_off[r] + p.req_loc_off[r];  // request-major item numbering
+    for (int c = 0; c < nc; ++c)
+      for (int g = 0; g < groups; ++g) {
+        ItemDesc d;
+        d.r = r;
+        d.w = min(kMaxItemBranches, w - g * kMaxItemBranches);
+        d.adm_off = adm_off + g * kMaxItemBranches;
+        d.cs0 = cs_r + c * w + g * kMaxItemBranches;
+        d.tb = c * kChunk; d.te = min(d.tb + kChunk, p.Lsh[r]);
+        d.nt = (d.te - d.tb + kTileTokens - 1) / kTileTokens;
+        d.flags = 0;
+        p.items[it0 + c * groups + g] = d;
+      }
+    // local items: per admitted branch, its local tiles in groups of kLocalItemTiles
+    const int l0 = p.req_loc_off[r];
+    int li = 0;
     for (int j = 0; j < w; ++j) {
       const int s = p.adm_by_req[adm_off + j];
       const int L = p.Lloc[s];
-      for (int t0 = 0; t0 < L; t0 += kTileTokens, ++lt)
-        p.ltiles[(size_t)(l0 + lt / kLocalItemTiles) * kLocalItemTiles + lt % kLocalItemTiles] =
-            make_int4(s, t0, min(kTileTokens, L - t0), j);
-    }
-    for (int li = 0; li < nl; ++li) {
-      ItemDesc d;
-      d.r = r; d.w = w; d.adm_off = adm_off; d.cs0 = cs_r + (nc + li) * w;
-      d.tb = (l0 + li) * kLocalItemTiles; d.te = 0;
-      d.nt = min(kLocalItemTiles, lt - li * kLocalItemTiles);
-      d.flags = 1 | (rep << 1) | (m64 << 4);
-      p.items[p.req_chunk_off[r] + l0 + nc + li] = d;
+      for (int t0 = 0; t0 < L; t0 += kTileTokens * kLocalItemTiles, ++li) {
+        const int nt = min(kLocalItemTiles, (L - t0 + kTileTokens - 1) / kTileTokens);
+        for (int t = 0; t < nt; ++t) {
+          const int tok = t0 + t * kTileTokens;
+          p.ltiles[(size_t)(l0 + li) * kLocalItemTiles + t] =
+              make_int4(s, tok, min(kTileTokens, L - tok), 0);
+        }
+        ItemDesc d;
+        d.r = r; d.w = 1; d.adm_off = adm_off + j; d.cs0 = cs_r + nc * w + li;
+        d.tb = (l0 + li) * kLocalItemTiles; d.te = 0;
+        d.nt = nt;
+        d.flags = 1;
+        p.items[it0 + nsh + li] = d;
+      }
     }
   }
   for (int i = tid; i < 2 * R * kGroup; i += blockDim.x) p.done[i] = 0;
@@ -408,11 +417,21 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     int s = tid * kPerThread + k;
     if (s < S && f[k]) {
       p.adm_list[fl[k]] = s;
-      const int r = p.slot_req[s];
-      const int nq = (p.req_chunk_off[r + 1] - p.req_chunk_off[r]) +
-                     (p.req_loc_off[r + 1] - p.req_loc_off[r]);
-      p.merge_desc[fl[k]] = make_int4(s, p.req_part_off[r] + p.slot_rank[s], nq,
-                                      (p.req_adm_off[r + 1] - p.req_adm_off[r]) | (r << 16));
+      // merge descriptor: the slot's shared partials (stride w) and its own local items'
+      const int r = p.slot_req[s], j = p.slot_rank[s];
+      const int w = p.req_adm_off[r + 1] - p.req_adm_off[r];
+      const int groups = (w + kMaxItemBranches - 1) / kMaxItemBranches;
+      const int nc = (p.req_chunk_off[r + 1] - p.req_chunk_off[r]) / groups;
+      const int n_items = (p.req_chunk_off[r + 1] - p.req_chunk_off[r]) +
+                          (p.req_loc_off[r + 1] - p.req_loc_off[r]);
+      int lpre = 0;  // local items of the request's branches before j
+      for (int jj = 0; jj < j; ++jj)
+        lpre += (p.Lloc[p.adm_by_req[p.req_adm_off[r] + jj]] + kTileTokens * kLocalItemTiles - 1) /
+                (kTileTokens * kLocalItemTiles);
+      const int nl = (p.Lloc[s] + kTileTokens * kLocalItemTiles - 1) / (kTileTokens * kLocalItemTiles);
+      const int cs_r = p.req_part_off[r];
+      p.merge_desc[2 * fl[k]] = make_int4(s, cs_r + j, nc, w);
+      p.merge_desc[2 * fl[k] + 1] = make_int4(cs_r + nc * w + lpre, nl, r, n_items);
     }
   }
   if (tid == 0) {

@@ -38,38 +38,34 @@ namespace taper {
 
 constexpr int kTile = kTileTokens;   // 64 tokens per pipeline stage
 // K and V tiles ride separate TMA rings: a K stage is released as soon as QK(t) completes,
-// a V stage only after PV(t); each stage is 64 tokens x 128 d bf16 = two 8 KB boxes.
-constexpr int kKStages = 6;
-constexpr int kVStages = 6;
+// a V stage only after PV(t); each stage is 64 tokens x 128 d bf16 = 16 KB.
+constexpr int kKStages = 5;
+constexpr int kVStages = 5;
 constexpr int kStageBytes = 2 * 8192;
-constexpr int kOffV = kKStages * kStageBytes;                 // 64 KB
-constexpr int kOffQS = kOffV + kVStages * kStageBytes;        // 160 KB: next item's queries
-constexpr int kQSRows = 64;                                   // staged rows per pass
-constexpr int kQSStride = 256 + 16;  // padded row stride: conflict-free 16 B row reads
-constexpr int kQSBytes = kQSRows * kQSStride;                 // 64 rows x 128 bf16
-constexpr int kXCols = 16;                                    // epilogue pass width
-constexpr int kXStride = kXCols + 4;                          // floats per staged row (+pad)
-constexpr int kOffX = kOffQS + kQSBytes;                      // epilogue staging 128 rows
-constexpr int kXBytes = 128 * kXStride * 4;
-constexpr int kOffML = kOffX + kXBytes;           // (m, l) of the 128 M-rows, 2 buffers
-constexpr int kItemRing = 8;                      // claimed-item ring (ItemRec, 512 B each)
-constexpr int kOffRec = kOffML + 2 * 128 * 8;
+constexpr int kOffV = kKStages * kStageBytes;
+constexpr int kOffQ = kOffV + kVStages * kStageBytes;   // Q^T operand, 2 buffers x 64 rows
+constexpr int kQBytes = kMaxItemBranches * kGroup * 256;  // 16 KB: [branch][d-half][8][128 B]
+constexpr int kOffPT = kOffQ + 2 * kQBytes;              // P^T operand: 128 rows x 128 B
+constexpr int kPTBytes = 2 * kMaxItemBranches * kGroup * 128;
+constexpr int kPTBufs = 1;  // a second buffer (decoupling PV(n-1) from softmax(n)) measured no gain
+constexpr int kOffML = kOffPT + kPTBufs * kPTBytes;  // (m, l) of the 64 stacked rows, 2 buffers
+// cross-warp reductions per softmax group: max [2 parities][4 warps][64], sum [4][64]
+constexpr int kRedFloats = 3 * 4 * 64;
+constexpr int kOffRed = kOffML + 2 * 64 * 8;
+constexpr int kOffAlpha = kOffRed + 2 * kRedFloats * 4;  // per-warp rescale factors [8][64]
+constexpr int kItemRing = 8;                  // claimed-item ring (ItemRec, 512 B each)
+constexpr int kOffRec = kOffAlpha + 8 * 64 * 4;
 constexpr int kOffBar = kOffRec + kItemRing * 512;
 constexpr int kSmemUsed = kOffBar + 512;
-constexpr int kSmemBytes = kSmemUsed + 1024;      // + alignment slack
-// warp 0: K producer; warp 1: MMA issuer; warps 2-5: softmax; warps 6-9: epilogue;
-// warp 10: V producer; warp 11: item scheduler (claims, resolves tiles, stages queries)
-constexpr int kAttnThreads = 384;
-constexpr int kRingConsumers = 11;  // warps 0-10 release every item record
+constexpr int kSmemBytes = kSmemUsed + 1024;  // + alignment slack
+// warp 0: K producer; warp 1: MMA issuer; warps 2-5: softmax group 0; warps 6-9:
+// epilogue; warp 10: V producer; warp 11: item scheduler (claims, resolves tiles, loads Q);
+// warps 12-15: softmax group 1.  A group owns 8-row blocks of the stacked rows.
+constexpr int kAttnThreads = 512;
+constexpr int kRingConsumers = 15;  // every warp but the scheduler releases each record
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColS = 0;     // S0 / P0 [0, 64), S1 / P1 [64, 128)
-constexpr uint32_t kColO = 128;   // O0 [128, 256), O1 [256, 384)
-constexpr uint32_t kColQ = 384;   // Q0 [384, 448), Q1 [448, 512): 128 bf16 per row, 64 packed cols
-
-constexpr uint32_t kIdescQK = umma_idesc_bf16(128, 64, false, false);
-constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, false, true);
-constexpr uint32_t kIdescQK64 = umma_idesc_bf16(64, 64, false, false);
-constexpr uint32_t kIdescPV64 = umma_idesc_bf16(64, 128, false, true);
+constexpr uint32_t kColS = 0;     // S^T 0 [0, 64), S^T 1 [64, 128): 64 tokens x N rows
+constexpr uint32_t kColO = 128;   // O^T 0 [128, 256), O^T 1 [256, 384): 128 d x 2N rows
 
 struct AttnParams {
   const int32_t *slot_page_off, *slot_pages, *req_page_off, *req_pages;
@@ -78,10 +74,9 @@ struct AttnParams {
   int32_t *done;       // [r * 8 + g]: items of (request, KV head) whose partials are written
   const ItemDesc *items;
   const int4 *ltiles;
-  const __nv_bfloat16 *q;
   float *part_lse, *part_o;
   int h_local, page_size;
-  int tma5d;  // 1: page_size >= 64, one 5-D box per tile; 0: two 4-D boxes per page
+  int tma5d;  // 1: page_size >= 64, one 5-D box per full tile; 0: 4-D boxes of one page
   float scale_log2;
   long long *trace;  // debug: pipeline event timestamps of CTA 0 (taper_set_trace_buffer)
   int trace_cap;
@@ -94,24 +89,16 @@ __device__ __forceinline__ void trace_ev(const AttnParams &p, int e, uint32_t n)
 }
 
 struct Item {
-  int r, g, local, w, adm_off, cs0, nt, tb, te, rep, m64;
+  int r, g, local, w, adm_off, cs0, nt, tb, te;
 };
 
-// TMEM row layout of the MMA accumulator (cta_group::1): M = 128 puts row m in lane m; M = 64
-// puts rows 16q..16q+15 in lanes 32q..32q+15 (16 rows per lane quadrant).  Returns the M-row
-// held by (quadrant wq, lane) or -1.
-__device__ __forceinline__ int mrow_of(int m64, int wq, int lane) {
-  if (!m64) return wq * 32 + lane;
-  return lane < 16 ? wq * 16 + lane : -1;
-}
-
 // A claimed work item as the scheduler warp resolves it into SMEM: the descriptor plus, per
-// 64-token tile, its first token, valid tokens, owning branch (-1: all rows) and the page of
-// each 16-token box.  Every other role reads only this record (no global loads per item).
+// 64-token tile, its first token, valid tokens and the page of each 16-token box.  Every
+// other role reads only this record (no global loads per item).
 struct ItemRec {
   int32_t it, g, desc[8];  // desc = ItemDesc {r, w, adm_off, cs0, tb, te, nt, flags}
   int32_t pad[6];
-  int32_t tok0[kLocalItemTiles], valid[kLocalItemTiles], jrow[kLocalItemTiles];
+  int32_t tok0[kLocalItemTiles], valid[kLocalItemTiles], spare[kLocalItemTiles];
   int32_t pg[kLocalItemTiles][4];
 };
 static_assert(sizeof(ItemRec) == 512, "ItemRec size");
@@ -120,15 +107,12 @@ __device__ __forceinline__ void decode_item(const ItemRec *rec, Item &x) {
   x.g = rec->g;
   x.r = rec->desc[0]; x.w = rec->desc[1]; x.adm_off = rec->desc[2]; x.cs0 = rec->desc[3];
   x.tb = rec->desc[4]; x.te = rec->desc[5]; x.nt = rec->desc[6];
-  const int f = rec->desc[7];
-  x.local = f & 1;
-  x.rep = (f >> 1) & 7;
-  x.m64 = (f >> 4) & 1;
+  x.local = rec->desc[7] & 1;
 }
 
 struct TileInfo {
   const int32_t *pages;
-  int tok0, valid, jrow;  // jrow = owning branch (local tiles) or -1 (all rows)
+  int tok0, valid;
 };
 
 __device__ __forceinline__ TileInfo tile_info(const AttnParams &p, const Item &x, int t) {
@@ -137,59 +121,13 @@ __device__ __forceinline__ TileInfo tile_info(const AttnParams &p, const Item &x
     ti.pages = p.req_pages + __ldg(p.req_page_off + x.r);
     ti.tok0 = x.tb + t * kTile;
     ti.valid = min(kTile, x.te - ti.tok0);
-    ti.jrow = -1;
   } else {
-    const int4 lt = __ldg(p.ltiles + x.tb + t);  // {slot, tok0, valid, branch}
+    const int4 lt = __ldg(p.ltiles + x.tb + t);  // {slot, tok0, valid, -}
     ti.pages = p.slot_pages + __ldg(p.slot_page_off + lt.x);
     ti.tok0 = lt.y;
     ti.valid = lt.z;
-    ti.jrow = lt.w;
   }
   return ti;
-}
-
-// valid tokens and owning branch of tile t (softmax side)
-__device__ __forceinline__ int2 tile_rows(const ItemRec *rec, int t) {
-  return make_int2(rec->valid[t], rec->jrow[t]);
-}
-
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// Move the item's staged stacked queries (SMEM, [row][128] bf16, filled by the producer's
-// bulk copies in passes of 64 rows) into TMEM columns [qcol, qcol + 64), replicated over
-// the row copies; each pass's buffer is released after use.  Ends with the tcgen05 stores
-// complete and fenced.  `pass` counts staging passes consumed so far (updated).
-__device__ __forceinline__ void stage_q_tmem(const Item &x, const uint8_t *qs, uint64_t *qs_full,
-                                             uint64_t *qs_free, uint32_t &pass, uint32_t tmem,
-                                             uint32_t lane_off, int wq, int lane, uint32_t qcol) {
-  const int R8 = 8 * x.w;
-  const int m = mrow_of(x.m64, wq, lane);
-  const int rpc = (x.m64 ? 64 : 128) / x.rep;
-  const int i = m >= 0 ? m % rpc : 1 << 20;
-  uint32_t v[64];
-#pragma unroll
-  for (int c = 0; c < 64; ++c) v[c] = 0u;
-  for (int r0 = 0; r0 < R8; r0 += kQSRows, ++pass) {
-    mbar_wait(qs_full, pass & 1);
-    if (i >= r0 && i < min(R8, r0 + kQSRows)) {
-      const uint4 *src = reinterpret_cast<const uint4 *>(qs + (i - r0) * kQSStride);
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const uint4 u = src[c];
-        v[4 * c] = u.x; v[4 * c + 1] = u.y; v[4 * c + 2] = u.z; v[4 * c + 3] = u.w;
-      }
-    }
-    mbar_arrive(qs_free);
-  }
-  tmem_st_n<64>(tmem + lane_off + qcol, v);
-  tmem_st_wait();
-  tc_fence_before();
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -200,135 +138,355 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
-// S[tS] = Q[tQ] * K^T: 8 k-steps of 16 over d = 128 (A = Q from TMEM, B = K tile in SMEM,
-// SW128 K-major: d 0..63 in the first 8 KB box, 64..127 in the second).
-__device__ __forceinline__ void issue_qk(uint32_t tS, uint32_t tQ, uint32_t kb, uint32_t idesc) {
-  const uint32_t nomask[4] = {0u, 0u, 0u, 0u};
-  const uint64_t b0 = umma_desc_sw128(kb, 16, 1024);
+// S^T[tS] = K Q^T ("swap-AB": tokens on M = 64, stacked rows on N = 8 wpad).  A = the K tile
+// (SW128 K-major: [d-half][64 tokens][64 d], halves 8 KB apart), B = Q^T (SW128 K-major:
+// [branch][d-half][8 rows][64 d], 8-row groups 2 KB apart, halves 1 KB apart); 8 k-steps of
+// 16 over d = 128.
+__device__ __forceinline__ void issue_qk(uint32_t tS, uint32_t kb, uint32_t qb, uint32_t idesc) {
+  const uint64_t a0 = umma_desc_sw128(kb, 16, 1024);
+  const uint64_t b0 = umma_desc_sw128(qb, 16, 2048);
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
-    const uint64_t b = b0 + uint64_t((((kk >> 2) * 8192) + (kk & 3) * 32) >> 4);
-    tc_mma_f16_ts(tS, tQ + kk * 8, b, idesc, kk > 0 ? 1u : 0u, nomask);
+    const uint64_t a = a0 + uint64_t((((kk >> 2) * 8192) + (kk & 3) * 32) >> 4);
+    const uint64_t b = b0 + uint64_t((((kk >> 2) * 1024) + (kk & 3) * 32) >> 4);
+    tc_mma_f16(tS, a, b, idesc, kk > 0 ? 1u : 0u);
   }
 }
 
-// O[tO] += P[tP] * V: P = hi (columns 0..31) + lo (32..63), 4 k-steps of 16 tokens;
-// B = V tile as an MN-major SW128 operand (d 0..63 / 64..127 boxes 8 KB apart).  With REP
-// replicated row copies, copy c owns tokens [c*64/REP, (c+1)*64/REP): its k-steps run
-// with the other copies' TMEM lanes masked off.
-template <int REP>
-__device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t vb, bool first,
+// O^T[tO] (+)= V^T P^T: M = 128 (d), N = 16 wpad (per branch: 8 hi rows then 8 lo rows of
+// P = hi + lo), K = 64 tokens in 4 k-steps.  A = the V tile as an MN-major SW128 operand
+// (d halves 8 KB apart, 8-token groups 1 KB apart), B = P^T (SW128 K-major, 8-row groups
+// 1 KB apart).
+__device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t vb, uint32_t pb, bool first,
                                          uint32_t idesc) {
-  const uint64_t b0 = umma_desc_sw128(vb, 8192, 1024);
-  constexpr int KPC = 4 / REP;
+  const uint64_t a0 = umma_desc_sw128(vb, 8192, 1024);
+  const uint64_t b0 = umma_desc_sw128(pb, 16, 1024);
 #pragma unroll
-  for (int c = 0; c < REP; ++c) {
-    uint32_t mask[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) mask[q] = (REP == 1 || q / (4 / REP) == c) ? 0u : 0xffffffffu;
-    constexpr int kParts = 2;  // P = hi + lo
-#pragma unroll
-    for (int part = 0; part < kParts; ++part) {
-#pragma unroll
-      for (int k = 0; k < KPC; ++k) {
-        const int kk = c * KPC + k;
-        const uint64_t b = b0 + uint64_t((kk * 2048) >> 4);
-        tc_mma_f16_ts(tO, tP + part * 32 + kk * 8, b, idesc,
-                      (first && part == 0 && k == 0) ? 0u : 1u, mask);
-      }
-    }
+  for (int kk = 0; kk < 4; ++kk) {
+    const uint64_t a = a0 + uint64_t((kk * 2048) >> 4);
+    const uint64_t b = b0 + uint64_t((kk * 32) >> 4);
+    tc_mma_f16(tO, a, b, idesc, (first && kk == 0) ? 0u : 1u);
   }
 }
 
-// One tile of the online softmax for a thread's row, branch-free.  CW = tokens of the tile
-// handled by this thread; nvalid = live tokens among them (0 for a row that is dead in this
-// tile).  Updates m_run and this thread's share of l_run, and writes P (hi, lo) into the
-// row's S columns.  M = 128 (SPLIT = false): one thread per row (TMEM lane), tokens
-// [colbase, colbase + CW).  M = 64 (SPLIT = true): rows live in lanes 0-15 of the quadrant and
-// two threads share a row -- lane t < 16 takes tokens [colbase, +CW), lane t + 16 the next CW
-// (16x32bx2 accesses); the row max is combined across the pair, the row sum at the end of
-// the item.
-template <int CW, bool SPLIT>
-__device__ __forceinline__ void softmax_tile(uint32_t tS, int colbase, int nvalid, bool o_live,
-                                             float c, float &m_run, float &l_run, uint32_t tO,
-                                             uint64_t *pv_prev, uint32_t pv_prev_parity) {
-  uint32_t s[CW];
-  if constexpr (SPLIT) {
-    if constexpr (CW == 8) tmem_ld_x2_8<CW>(tS + colbase, s);
-    else if constexpr (CW == 16) tmem_ld_x2_16<CW>(tS + colbase, s);
-    else tmem_ld_x2_32<CW>(tS + colbase, s);
+// 16 TMEM lanes x 8 wpad columns in the 16x256b pattern: for column block b, registers
+// 4b..4b+3 hold (token lane/4, col 8b + 2(lane%4)), (same, +1), (token lane/4 + 8, col),
+// (same, +1) -- the mma.m16n8 accumulator fragment.
+template <int WPAD>
+__device__ __forceinline__ void tmem_ld_16x256(uint32_t taddr, uint32_t (&v)[4 * WPAD]) {
+  if constexpr (WPAD == 1) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(taddr));
+  } else if constexpr (WPAD == 2) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                   "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+  } else if constexpr (WPAD == 3) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                   "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]) : "r"(taddr + 16));
+  } else if constexpr (WPAD == 4) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
   } else {
-    tmem_ld_n<CW>(tS + colbase, s);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
   }
-  tmem_ld_wait();
-  float x[CW];
+}
+
+__device__ __forceinline__ void stmatrix_x4_trans(uint32_t addr, uint32_t r0, uint32_t r1,
+                                                  uint32_t r2, uint32_t r3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+               "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t *>(&h2);
+}
+
+// Butterfly plan for NC columns over lane bits 4, 3, 2: an even count is halved by a
+// transposing exchange (each lane keeps one half), an odd one is reduced in place.
+__host__ __device__ constexpr int bfly_cnt(int nc, int st) {
+  int c = nc;
+  for (int i = 0; i < st; ++i) c = (c % 2 == 0) ? c / 2 : c;
+  return c;
+}
+
+struct SoftmaxCtx {  // per-thread constants of a softmax warp
+  const AttnParams *p;
+  uint8_t *smem;
+  uint64_t *s_full, *pv_done, *vfull, *p_full_g, *o_free, *ml_full;
+  float2 *xml;
+  float *red_g, *alpha_s;
+  uint32_t tmem, lane_off, pt_base;
+  int grp, wq, lane, warp, tid, bar_id;
+  float c;
+};
+
+// One item of a softmax group in the transposed layout.  This thread holds tokens
+// tA = lane/4 and tA + 8 of its warp's 16-token slice and, per 8-row block b < WB of the
+// group's blocks [blk0, blk0 + WB), stacked rows 8 (blk0 + b) + 2 (lane%4) + {0, 1}
+// (column index i = 2b + e).  Running max (lazy: moves only when a tile's max exceeds it
+// by > 8 in log2 units) and this thread's partial row sums live in registers.  Column max
+// per tile: a transposing butterfly over the 8 lanes sharing columns, one SMEM exchange
+// across the group's 4 warps for the columns a lane ends up owning, the lazy update there,
+// and the mirrored butterfly broadcasting the maxima back.  P = hi + lo (bf16 each) goes to
+// SMEM as P^T (the PV MMA's B operand) via stmatrix.trans once PV(n-1) has released it.
+// WB = 0: the group has no rows in this item and only keeps the barrier phases in step.
+template <int WB>
+__device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec *rec, const Item &x,
+                                             int blk0, uint32_t item_idx, uint32_t &n) {
+  constexpr int NC = WB > 0 ? 2 * WB : 2;    // columns per thread
+  constexpr int NF = bfly_cnt(NC, 3);        // columns a lane owns after the butterfly
+  const int lane = C.lane, wq = C.wq;
+  const int c0 = 2 * (lane & 3);
+  const int tA = 16 * wq + (lane >> 2);      // token within the 64-token tile
+  const uint32_t ob = item_idx & 1;
+  const uint32_t tO = C.tmem + C.lane_off + kColO + ob * 128;
+  const int n_live = 8 * x.w;
+  // lane-invariant butterfly ownership and stmatrix addresses
+  int off = 0;
 #pragma unroll
-  for (int j = 0; j < CW; ++j) x[j] = j < nvalid ? __uint_as_float(s[j]) : -INFINITY;
-  float mx = x[0];
-#pragma unroll
-  for (int j = 1; j < CW; ++j) mx = fmaxf(mx, x[j]);
-  if constexpr (SPLIT) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-  mx *= c;  // scores in log2 units (c = softmax scale * log2 e > 0)
-  // lazy rescale: only raise the running max when it grows by more than 8 (log2 units)
-  const bool need = mx > m_run + 8.f;
-  float alpha = 1.f;
-  if (need) {
-    alpha = ex2(m_run - mx);  // 0 when m_run = -inf
-    l_run *= alpha;
-    m_run = mx;
+  for (int st = 0; st < 3; ++st) {
+    const int cnt = bfly_cnt(NC, st);
+    if (cnt % 2 == 0 && (lane & (16 >> st))) off += cnt / 2;
   }
-  if (o_live && __any_sync(0xffffffffu, need)) {
-    mbar_wait(pv_prev, pv_prev_parity);  // O *= alpha needs PV(n-1) complete
+  int col[NF];
+#pragma unroll
+  for (int j = 0; j < NF; ++j) col[j] = 8 * ((off + j) >> 1) + c0 + ((off + j) & 1);
+  uint32_t st_addr[WB > 0 ? WB : 1];
+  {
+    const int mi = lane >> 3, k = lane & 7;
+    const int ch = 2 * wq + (mi & 1);
+#pragma unroll
+    for (int b = 0; b < WB; ++b) {
+      const int R = 16 * (blk0 + b) + ((mi >> 1) << 3) + k;
+      st_addr[b] = C.pt_base + (R >> 3) * 1024 + (R & 7) * 128 + (((ch ^ (R & 7)) & 7) << 4);
+    }
+  }
+  const bool rows_live = 8 * (blk0 + WB) <= n_live;
+  float m_run[NC], l_run[NC], m_red[NF];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) { m_run[i] = -INFINITY; l_run[i] = 0.f; }
+#pragma unroll
+  for (int j = 0; j < NF; ++j) m_red[j] = -INFINITY;
+
+  for (int t = 0; t < x.nt; ++t) {
+    const uint32_t sb = n & 1;
+    const int nvalid = x.local ? rec->valid[t] : min(kTile, x.te - (x.tb + t * kTile));
+    mbar_wait(C.s_full + sb, (n >> 1) & 1);
+    if (C.warp == 2 && lane == 0) trace_ev(*C.p, 7, n);
     tc_fence_after();
-#pragma unroll 1
-    for (int q = 0; q < (SPLIT ? 2 : 4); ++q) {
-      uint32_t o[32];
-      if constexpr (SPLIT) tmem_ld_x2_32<64>(tO + q * 32, o);
-      else tmem_ld32(tO + q * 32, o);
+    if constexpr (WB > 0) {
+      const uint32_t tS = C.tmem + C.lane_off + kColS + sb * 64;
+      float *red_max = C.red_g + (n & 1) * 256;
+      uint32_t s[4 * WB];
+      tmem_ld_16x256<WB>(tS + 8 * blk0, s);
       tmem_ld_wait();
+      float x2[4 * WB];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-      if constexpr (SPLIT) tmem_st_x2_32<64>(tO + q * 32, o);
-      else tmem_st32(tO + q * 32, o);
-    }
-    tmem_st_wait();
-  }
-  // P = 2^(x - m) split into hi + lo bf16 (DESIGN.md Sec. 6 "P precision"), written back
-  // into this row's S columns in groups of up to 16 tokens (8 packed columns per part)
-  constexpr int G = CW < 16 ? CW : 16;
-  const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
-  float lsum = 0.f;
+      for (int i = 0; i < 4 * WB; ++i) x2[i] = __uint_as_float(s[i]);
+      if (nvalid < kTile || !rows_live) {
+        const bool vA = tA < nvalid, vB = tA + 8 < nvalid;
 #pragma unroll
-  for (int g = 0; g < CW / G; ++g) {
-    uint32_t hi[G / 2], lo[G / 2];
+        for (int b = 0; b < WB; ++b)
 #pragma unroll
-    for (int jj = 0; jj < G / 2; ++jj) {
-      const int j = g * (G / 2) + jj;
-      const float e0 = ex2(fmaf(x[2 * j], c, neg_m));
-      const float e1 = ex2(fmaf(x[2 * j + 1], c, neg_m));
-      lsum += e0 + e1;
-      const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
-      const float2 f2 = __bfloat1622float2(h2);
-      const __nv_bfloat162 l2 = __floats2bfloat162_rn(e0 - f2.x, e1 - f2.y);
-      hi[jj] = *reinterpret_cast<const uint32_t *>(&h2);
-      lo[jj] = *reinterpret_cast<const uint32_t *>(&l2);
-    }
-    const uint32_t col = colbase / 2 + g * (G / 2);
-    if constexpr (SPLIT) {
-      if constexpr (G == 8) {
-        tmem_st_x2_4<CW / 2>(tS + col, hi);
-        tmem_st_x2_4<CW / 2>(tS + 32 + col, lo);
-      } else {
-        tmem_st_x2_8<CW / 2>(tS + col, hi);
-        tmem_st_x2_8<CW / 2>(tS + 32 + col, lo);
+          for (int e = 0; e < 2; ++e) {
+            const bool live = 8 * (blk0 + b) + c0 + e < n_live;
+            if (!(live && vA)) x2[4 * b + e] = -INFINITY;
+            if (!(live && vB)) x2[4 * b + 2 + e] = -INFINITY;
+          }
       }
-    } else {
-      tmem_st8(tS + col, hi);
-      tmem_st8(tS + 32 + col, lo);
+      float v[NC];
+#pragma unroll
+      for (int i = 0; i < NC; ++i) v[i] = fmaxf(x2[4 * (i >> 1) + (i & 1)], x2[4 * (i >> 1) + 2 + (i & 1)]);
+#pragma unroll
+      for (int st = 0; st < 3; ++st) {
+        const int M = 16 >> st;
+        const int cnt = bfly_cnt(NC, st);
+        if (cnt % 2 == 0) {
+          const bool up = (lane & M) != 0;
+#pragma unroll
+          for (int j = 0; j < cnt / 2; ++j) {
+            const float send = up ? v[j] : v[cnt / 2 + j];
+            const float keep = up ? v[cnt / 2 + j] : v[j];
+            v[j] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, M));
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < cnt; ++j) v[j] = fmaxf(v[j], __shfl_xor_sync(0xffffffffu, v[j], M));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NF; ++j) red_max[wq * 64 + col[j]] = v[j];
+      named_bar_sync(C.bar_id, 128);
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        float mx = fmaxf(fmaxf(red_max[col[j]], red_max[64 + col[j]]),
+                         fmaxf(red_max[128 + col[j]], red_max[192 + col[j]]));
+        mx *= C.c;  // log2 units (c = softmax scale * log2 e > 0)
+        if (mx > m_red[j] + 8.f) m_red[j] = mx;
+        v[j] = m_red[j];
+      }
+#pragma unroll
+      for (int st = 2; st >= 0; --st) {
+        const int M = 16 >> st;
+        const int cnt = bfly_cnt(NC, st);
+        if (cnt % 2 == 0) {
+          const bool up = (lane & M) != 0;
+          float lo[NC], hi[NC];
+#pragma unroll
+          for (int j = 0; j < cnt / 2; ++j) {
+            const float recv = __shfl_xor_sync(0xffffffffu, v[j], M);
+            lo[j] = up ? recv : v[j];
+            hi[j] = up ? v[j] : recv;
+          }
+#pragma unroll
+          for (int j = 0; j < cnt / 2; ++j) { v[j] = lo[j]; v[cnt / 2 + j] = hi[j]; }
+        }
+      }
+      bool need_any = false;
+      float alpha[NC];
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        alpha[i] = 1.f;
+        if (v[i] != m_run[i]) {
+          alpha[i] = ex2(m_run[i] - v[i]);  // 0 when m_run = -inf
+          l_run[i] *= alpha[i];
+          m_run[i] = v[i];
+          need_any = true;
+        }
+      }
+      // P = 2^(x c - m) = hi + lo (bf16 each), packed for stmatrix before waiting on the MMA
+      uint32_t pk[4 * WB];
+#pragma unroll
+      for (int b = 0; b < WB; ++b) {
+        float pA[2], pB[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = 2 * b + e;
+          const float neg_m = m_run[i] == -INFINITY ? 0.f : -m_run[i];
+          pA[e] = ex2(fmaf(x2[4 * b + e], C.c, neg_m));
+          pB[e] = ex2(fmaf(x2[4 * b + 2 + e], C.c, neg_m));
+          l_run[i] += pA[e] + pB[e];
+        }
+        const uint32_t hA = pack_bf16(pA[0], pA[1]), hB = pack_bf16(pB[0], pB[1]);
+        const float2 fA = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&hA));
+        const float2 fB = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&hB));
+        pk[4 * b] = hA;
+        pk[4 * b + 1] = hB;
+        pk[4 * b + 2] = pack_bf16(pA[0] - fA.x, pA[1] - fA.y);
+        pk[4 * b + 3] = pack_bf16(pB[0] - fB.x, pB[1] - fB.y);
+      }
+      // the P^T buffer this tile writes was last read by PV(n - kPTBufs); an O rescale
+      // needs PV(n-1) complete
+      const bool rescale = t > 0 && __any_sync(0xffffffffu, need_any);
+      if ((rescale || kPTBufs == 1) && n >= 1)
+        mbar_wait(C.pv_done + ((n - 1) & 1), ((n - 1) >> 1) & 1);
+      else if (n >= 2)
+        mbar_wait(C.pv_done + (n & 1), ((n - 2) >> 1) & 1);
+      if (rescale) {
+        // O^T *= alpha for the group's rows: every warp holds every factor (lanes 0-3 cover
+        // all of the group's columns), published in the warp's own SMEM slice
+        if (lane < 4) {
+#pragma unroll
+          for (int b = 0; b < WB; ++b) {
+            C.alpha_s[8 * b + c0] = alpha[2 * b];
+            C.alpha_s[8 * b + c0 + 1] = alpha[2 * b + 1];
+          }
+        }
+        __syncwarp();
+        tc_fence_after();
+#pragma unroll 1
+        for (int b = 0; b < WB; ++b) {
+          uint32_t o[16];
+          tmem_ld16(tO + 16 * (blk0 + b), o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            o[j] = __float_as_uint(__uint_as_float(o[j]) * C.alpha_s[8 * b + (j & 7)]);
+          tmem_st16(tO + 16 * (blk0 + b), o);
+        }
+        tmem_st_wait();
+      }
+      const uint32_t pbuf = (n % kPTBufs) * kPTBytes;
+#pragma unroll
+      for (int b = 0; b < WB; ++b)
+        stmatrix_x4_trans(st_addr[b] + pbuf, pk[4 * b], pk[4 * b + 1], pk[4 * b + 2], pk[4 * b + 3]);
+    } else if (n >= uint32_t(kPTBufs)) {  // no rows: keep in step with the writers
+      mbar_wait(C.pv_done + ((n - kPTBufs) & 1), ((n - kPTBufs) >> 1) & 1);
     }
+    if (C.grp == 0 && nvalid < kTile) {
+      // partial tile: V rows past the last valid token were not loaded (or hold tokens
+      // past the sequence end); zero them so 0 * garbage cannot reach O
+      const uint32_t vs = n % kVStages;
+      mbar_wait(C.vfull + vs, (n / kVStages) & 1);
+      uint8_t *vt = C.smem + kOffV + vs * kStageBytes;
+      const int nz = (kTile - nvalid) * 8;  // 16 B chunks per d-half (128 B per row)
+      for (int i = C.tid - 64; i < 2 * nz; i += 128) {
+        const int hf = i / nz, j = i - hf * nz;
+        *reinterpret_cast<uint4 *>(vt + hf * 8192 + nvalid * 128 + j * 16) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    fence_proxy_async_smem();  // P^T / V zeros (generic stores) -> visible to the MMA
+    tc_fence_before();
+    if (lane == 0 && C.warp == 2) trace_ev(*C.p, 8, n);
+    mbar_arrive(C.p_full_g + (n & 1));
+    ++n;
   }
-  l_run += lsum;
-  tmem_st_wait();
+  // row sums: this thread's partial over its 2 tokens per tile -> 16 tokens -> 4 warps
+  float *red_sum = C.red_g + 512;
+  if constexpr (WB > 0) {
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      l_run[i] += __shfl_xor_sync(0xffffffffu, l_run[i], 4);
+      l_run[i] += __shfl_xor_sync(0xffffffffu, l_run[i], 8);
+      l_run[i] += __shfl_xor_sync(0xffffffffu, l_run[i], 16);
+    }
+    if (lane < 4) {
+#pragma unroll
+      for (int b = 0; b < WB; ++b) {
+        red_sum[wq * 64 + 8 * b + c0] = l_run[2 * b];
+        red_sum[wq * 64 + 8 * b + c0 + 1] = l_run[2 * b + 1];
+      }
+    }
+    named_bar_sync(C.bar_id, 128);
+  }
+  // publish (m, l) for the epilogue; xml[ob] was consumed by epilogue item_idx-2
+  mbar_wait(C.o_free + ob, ((item_idx >> 1) & 1) ^ 1);
+  if constexpr (WB > 0) {
+    if (wq == 0 && lane < 4) {
+#pragma unroll
+      for (int b = 0; b < WB; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cl = 8 * b + c0 + e;
+          const float L = red_sum[cl] + red_sum[64 + cl] + red_sum[128 + cl] + red_sum[192 + cl];
+          C.xml[ob * 64 + 8 * blk0 + cl] = make_float2(m_run[2 * b + e], L);
+        }
+    }
+    named_bar_sync(C.bar_id, 128);  // red_sum reused by the next item
+  }
+  mbar_arrive(C.ml_full + ob);
 }
 
 // Consumer side of the claimed-item ring: the k-th item this CTA processes (-1 = done).
@@ -344,7 +502,9 @@ __device__ __forceinline__ void ring_release(uint64_t *it_empty, uint32_t k, int
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attend_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                  AttnParams p) {
+                  const __grid_constant__ CUtensorMap tmK16,
+                  const __grid_constant__ CUtensorMap tmV16,
+                  const __grid_constant__ CUtensorMap tmQ, AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment (SW128) by pointer arithmetic on the shared array, so the compiler
   // keeps the shared address space (LDS/STS instead of generic loads)
@@ -355,50 +515,47 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t *vfull = kempty + kKStages;         // [kVStages] TMA -> MMA (V tile landed)
   uint64_t *vempty = vfull + kVStages;         // [kVStages] PV done -> TMA
   uint64_t *s_full = vempty + kVStages;        // [2] QK done -> softmax
-  uint64_t *p_full = s_full + 2;           // [2] softmax -> PV
-  uint64_t *pv_done = p_full + 2;          // [2] PV done -> softmax (O rescale)
-  uint64_t *q_full = pv_done + 2;          // softmax (Q staged) -> MMA
-  uint64_t *o_full = q_full + 1;           // [2] last PV of an item -> epilogue
-  uint64_t *o_free = o_full + 2;           // [2] epilogue done -> MMA / softmax
-  uint64_t *ml_full = o_free + 2;          // [2] softmax (m, l) published -> epilogue
-  uint64_t *qs_full = ml_full + 2;         // producer's Q staging copy landed
-  uint64_t *qs_free = qs_full + 1;         // softmax moved the staged Q into TMEM
-  uint64_t *it_full = qs_free + 1;         // [kItemRing] scheduler published an item record
-  uint64_t *it_empty = it_full + kItemRing;  // [kItemRing] all consumer warps are done with it
-  uint64_t *sched_go = it_empty + kItemRing;  // K producer started an item -> scheduler
+  uint64_t *p_full = s_full + 2;               // [group][tile parity] P^T written -> PV
+  uint64_t *pv_done = p_full + 4;              // [2] PV done -> softmax (P^T free, O stable)
+  uint64_t *q_full = pv_done + 2;              // [2] Q^T landed (TMA) -> MMA
+  uint64_t *q_free = q_full + 2;               // [2] last QK of the item done -> scheduler
+  uint64_t *o_full = q_free + 2;               // [2] last PV of an item -> epilogue
+  uint64_t *o_free = o_full + 2;               // [2] epilogue done -> MMA / softmax
+  uint64_t *ml_full = o_free + 2;              // [2] softmax (m, l) published -> epilogue
+  uint64_t *it_full = ml_full + 2;             // [kItemRing] scheduler published an item
+  uint64_t *it_empty = it_full + kItemRing;    // [kItemRing] all consumer warps are done
+  uint64_t *sched_go = it_empty + kItemRing;   // K producer started an item -> scheduler
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sched_go + 1);
   ItemRec *recs = reinterpret_cast<ItemRec *>(smem + kOffRec);
-  float *xo = reinterpret_cast<float *>(smem + kOffX);
   float2 *xml = reinterpret_cast<float2 *>(smem + kOffML);
+  float *red = reinterpret_cast<float *>(smem + kOffRed);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int h = p.h_local;
-  const int n_items = (__ldg(p.hdr) + __ldg(p.hdr + 5)) * h;
   if (p.trace != nullptr && tid == 0) {  // per-CTA wall-clock span (debug trace)
     unsigned long long g;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
     p.trace[(size_t)(3000 + blockIdx.x) * 16 + 0] = (long long)g;
   }
 
-  // Zero the K/V rings once: rows of a partial tile that TMA does not load must hold finite
-  // values (P = 0 there, but 0 * NaN would still poison O).
-  for (int i = tid; i < kOffQS / 16; i += kAttnThreads)
+  // Zero the K/V rings once: token rows of a partial tile that TMA does not load must hold
+  // finite values (P = 0 there, but 0 * NaN would still poison O).
+  for (int i = tid; i < kOffQ / 16; i += kAttnThreads)
     reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
   fence_proxy_async_smem();
   if (tid == 0) {
     for (int i = 0; i < kKStages; ++i) { mbar_init(kfull + i, 1); mbar_init(kempty + i, 1); }
     for (int i = 0; i < kVStages; ++i) { mbar_init(vfull + i, 1); mbar_init(vempty + i, 1); }
+    for (int i = 0; i < 4; ++i) mbar_init(p_full + i, 128);
     for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + i, 1);
-      mbar_init(p_full + i, 128);
       mbar_init(pv_done + i, 1);
+      mbar_init(q_full + i, 1);
+      mbar_init(q_free + i, 1);
       mbar_init(o_full + i, 1);
       mbar_init(o_free + i, 128);
-      mbar_init(ml_full + i, 128);
+      mbar_init(ml_full + i, 256);
     }
-    mbar_init(q_full, 128);
-    mbar_init(qs_full, 1);
-    mbar_init(qs_free, 128);
     for (int i = 0; i < kItemRing; ++i) {
       mbar_init(it_full + i, 1);
       mbar_init(it_empty + i, kRingConsumers);
@@ -407,7 +564,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
-  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmK); tma_prefetch_desc(&tmV); }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmK); tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmK16); tma_prefetch_desc(&tmV16); tma_prefetch_desc(&tmQ);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -421,14 +581,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // ======================= item scheduler ==================================================
     // Claims work items (global atomic counter -> dynamic scheduling) one item ahead of the
     // K producer, resolves each into an SMEM ItemRec (descriptor, tile geometry, page
-    // indices: lane l resolves tile l), publishes it, then stages the item's stacked queries
-    // (w slots x 8 heads x 256 B, 2 KB per slot) into SMEM by bulk copies in passes of 8
-    // slots for the softmax warps.  The dependent global loads of an item thus overlap the
-    // previous item instead of stalling the pipeline at every item boundary.
+    // indices: lane l resolves tile l), publishes it, then loads the item's stacked queries
+    // Q^T (one 2 KB TMA box per branch: its 8 GQA rows, SW128) into Q buffer k & 1.  The
+    // dependent global loads of an item thus overlap the previous item.
     const int box_tok = p.page_size < kTile ? p.page_size : kTile;
-    const int n_items = (__ldg(p.hdr) + __ldg(p.hdr + 5)) * p.h_local;
+    const int n_desc = __ldg(p.hdr) + __ldg(p.hdr + 5);
+    const int n_items = n_desc * h;
     int *work_counter = p.hdr + 8;
-    uint32_t qs_pass = 0;
     for (uint32_t k = 0;; ++k) {
       if (k >= 1) mbar_wait(sched_go, (k - 1) & 1);  // K producer started item k-1
       int it = 0;
@@ -440,8 +599,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_wait(it_empty + slot, ((k / kItemRing) & 1) ^ 1);
       int w = 0, adm_off = 0, g = 0;
       if (it >= 0) {
-        const int q = it / p.h_local;
-        g = it - q * p.h_local;
+        const int q = it / h;  // request-major: consecutive claims share a request's pages
+        g = it - q * h;
         const int32_t d = lane < 8 ? __ldg(reinterpret_cast<const int32_t *>(p.items + q) + lane) : 0;
         const int nt = __shfl_sync(0xffffffffu, d, 6);
         Item x;
@@ -456,7 +615,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           const TileInfo ti = tile_info(p, x, lane);
           rec->tok0[lane] = ti.tok0;
           rec->valid[lane] = ti.valid;
-          rec->jrow[lane] = ti.jrow;
 #pragma unroll
           for (int b = 0; b < kTile / 16; ++b)
             rec->pg[lane][b] =
@@ -467,23 +625,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(it_full + slot);  // release: the record is visible
       if (it < 0) break;
+      // Q^T of the item's w branches: box {64 d, 8 rows, 2 d-halves} of q viewed as
+      // (d-lo, GQA row, d-half, slot * h + g) -> [d-half][8 rows][128 B] per branch
+      const uint32_t qb = k & 1;
+      mbar_wait(q_free + qb, ((k >> 1) & 1) ^ 1);
       const int slot_j = lane < w ? __ldg(p.adm_by_req + adm_off + lane) : 0;
-      for (int j0 = 0; j0 < w; j0 += kQSRows / 8, ++qs_pass) {
-        const int nj = min(kQSRows / 8, w - j0);
-        mbar_wait(qs_free, (qs_pass & 1) ^ 1);
-        if (elect_one()) mbar_arrive_expect_tx(qs_full, nj * 2048);
-        __syncwarp();
-        // one 256 B copy per stacked row (slot j, head e) into the padded staging rows
-        for (int rr = lane; rr < kQSRows; rr += 32) {
-          const int j = rr >> 3;
-          const int s_j = __shfl_sync(0xffffffffu, slot_j, min(j0 + j, 31));
-          if (j < nj)
-            bulk_g2s(smem + kOffQS + rr * kQSStride,
-                     p.q + ((size_t)s_j * (kGroup * p.h_local) + g * kGroup + (rr & 7)) * kHeadDim,
-                     256, qs_full);
-        }
-        __syncwarp();
-      }
+      if (elect_one()) mbar_arrive_expect_tx(q_full + qb, w * 2048);
+      __syncwarp();
+      if (lane < w)
+        tma_load_4d(smem + kOffQ + qb * kQBytes + lane * 2048, &tmQ, q_full + qb, 0, 0, 0,
+                    slot_j * h + g);
+      __syncwarp();
     }
   } else if (warp == 0 || warp == 10) {
     // ======================= TMA producers: warp 0 = K, warp 10 = V =======================
@@ -491,6 +643,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // loop with warp-uniform operands and one elected lane issues (no waterfall loops).
     const bool is_k = warp == 0;
     const CUtensorMap *tmap = is_k ? &tmK : &tmV;
+    const CUtensorMap *tmap16 = is_k ? &tmK16 : &tmV16;
     uint64_t *ring_full = is_k ? kfull : vfull;
     uint64_t *ring_empty = is_k ? kempty : vempty;
     const int n_stages = is_k ? kKStages : kVStages;
@@ -518,7 +671,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
         for (int b = 0; b < kTile / 16; ++b) pg[b] = rec->pg[t][b];
         const uint32_t st = n_prod % n_stages;
-        const int n_box = (valid + box_tok - 1) / box_tok;
         uint8_t *dst = ring + st * kStageBytes;
         mbar_wait(ring_empty + st, ((n_prod / n_stages) & 1) ^ 1);
         if (is_k && lane == 0) trace_ev(p, 0, n_prod);
@@ -528,11 +680,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           p.trace[(size_t)(3000 + blockIdx.x) * 16 + 2] = (long long)g;  // first TMA issued
         }
         if (elect_one()) {
-          if (p.tma5d) {
+          if (p.tma5d && valid == kTile) {
             // one box: {64 d, 64 tokens, 2 d-halves} -> [d-half][token][64] (two SW128 atoms)
             mbar_arrive_expect_tx(ring_full + st, 2 * kTile * 128);
             tma_load_5d(dst, tmap, ring_full + st, 0, tok0 % p.page_size, 0, g_u, pg[0]);
+          } else if (p.tma5d) {
+            // partial tile: {64 d, 16 tokens} boxes per d-half up to the last valid token
+            // (rows past it are zeroed by the softmax warps before PV)
+            const int n16 = (valid + 15) >> 4;
+            mbar_arrive_expect_tx(ring_full + st, n16 * 2 * 2048);
+            for (int b = 0; b < n16; ++b)
+              for (int hf = 0; hf < 2; ++hf)
+                tma_load_5d(dst + hf * 8192 + b * 2048, tmap16, ring_full + st, 0,
+                            tok0 % p.page_size + 16 * b, hf, g_u, pg[0]);
           } else {
+            const int n_box = (valid + box_tok - 1) / box_tok;
             mbar_arrive_expect_tx(ring_full + st, n_box * half_box_bytes * 2);
 #pragma unroll
             for (int b = 0; b < kTile / 16; ++b) {
@@ -555,258 +717,162 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // Every lane runs the loop so all operands stay warp-uniform (uniform registers); the
     // tcgen05.mma / commit instructions are issued by elect.sync's lane (CUTLASS pattern).
     const uint32_t sK = smem_u32(smem), sV = smem_u32(smem + kOffV);
+    const uint32_t sQ = smem_u32(smem + kOffQ), sPT = smem_u32(smem + kOffPT);
     const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
-    uint32_t n = 0;  // global tile counter (S/P double buffer index = n & 1)
+    uint32_t n = 0;  // global tile counter (S double buffer index = n & 1)
     for (uint32_t item_idx = 0;; ++item_idx) {
       const int it = ring_item(it_full, recs, item_idx);
       Item x;
       decode_item(recs + item_idx % kItemRing, x);
       ring_release(it_empty, item_idx, lane);
       if (it < 0) break;
-      const int rep = __shfl_sync(0xffffffffu, x.rep, 0);
-      const int m64 = __shfl_sync(0xffffffffu, x.m64, 0);
-      const uint32_t idesc_qk = m64 ? kIdescQK64 : kIdescQK;
-      const uint32_t idesc_pv = m64 ? kIdescPV64 : kIdescPV;
+      const int wi = __shfl_sync(0xffffffffu, x.w, 0);
+      const int nt = __shfl_sync(0xffffffffu, x.nt, 0);
+      const uint32_t idesc_qk = umma_idesc_bf16(64, 8 * wi, false, false);
+      const uint32_t idesc_pv = umma_idesc_bf16(128, 16 * wi, true, false);
+      const uint32_t qb = item_idx & 1;
       const uint32_t ob = item_idx & 1;  // O double buffer
       const uint32_t tO = tmem_u + kColO + ob * 128;
-      mbar_wait(q_full, item_idx & 1);
+      mbar_wait(q_full + qb, (item_idx >> 1) & 1);
       if (lane == 0) trace_ev(p, 6, n);
       tc_fence_after();
-      for (int t = 0; t <= x.nt; ++t) {
-        if (t < x.nt) {
+      for (int t = 0; t <= nt; ++t) {
+        if (t < nt) {
           const uint32_t ks = n % kKStages;
           mbar_wait(kfull + ks, (n / kKStages) & 1);
           if (lane == 0) trace_ev(p, 1, n);
           tc_fence_after();
           if (elect_one()) {
-            issue_qk(tmem_u + kColS + (n & 1) * 64, tmem_u + kColQ + (item_idx & 1) * 64,
-                     sK + ks * kStageBytes, idesc_qk);
+            issue_qk(tmem_u + kColS + (n & 1) * 64, sK + ks * kStageBytes, sQ + qb * kQBytes,
+                     idesc_qk);
             tc_commit(kempty + ks);
             tc_commit(s_full + (n & 1));
+            if (t == nt - 1) tc_commit(q_free + qb);
           }
           __syncwarp();
           if (lane == 0) trace_ev(p, 2, n);
         }
         if (t > 0) {
-          // PV of the previous tile (its P is ready once the softmax arrives on p_full)
+          // PV of the previous tile (its P^T is ready once the softmax arrives on p_full)
           const uint32_t m = n - 1;
           mbar_wait(p_full + (m & 1), (m >> 1) & 1);
+          mbar_wait(p_full + 2 + (m & 1), (m >> 1) & 1);
           if (lane == 0) trace_ev(p, 3, m);
-          const bool first = (t == 1);
+          const bool first = t == 1;
+          if (first) mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);  // epilogue item-2 done
           const uint32_t vs = m % kVStages;
-          // O[ob] is free once the epilogue of item item_idx - 2 has read it
-          if (first) mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);
           mbar_wait(vfull + vs, (m / kVStages) & 1);
           tc_fence_after();
           if (elect_one()) {
-            const uint32_t tP = tmem_u + kColS + (m & 1) * 64;
-            const uint32_t vb = sV + vs * kStageBytes;
-            if (rep == 4) issue_pv<4>(tO, tP, vb, first, idesc_pv);
-            else if (rep == 2) issue_pv<2>(tO, tP, vb, first, idesc_pv);
-            else issue_pv<1>(tO, tP, vb, first, idesc_pv);
+            issue_pv(tO, sV + vs * kStageBytes, sPT + (m % kPTBufs) * kPTBytes, first, idesc_pv);
             tc_commit(vempty + vs);
             tc_commit(pv_done + (m & 1));
-            if (t == x.nt) tc_commit(o_full + ob);
+            if (t == nt) tc_commit(o_full + ob);
           }
           __syncwarp();
           if (lane == 0) trace_ev(p, 5, m);
         }
-        if (t < x.nt) ++n;
+        if (t < nt) ++n;
       }
     }
-  } else if (warp < 6) {
-    // ======================= softmax / O correction (128 threads) =======================
-    const int wq = warp & 3;            // TMEM lane quadrant of this warp
-    const uint32_t lane_off = uint32_t(wq * 32) << 16;
-    const float c_log2 = p.scale_log2;
-    uint32_t qs_pass = 0;
+  } else if (warp < 6 || warp >= 12) {
+    // ======================= softmax / O correction (2 groups x 128 threads) ==========
+    // Group 0 (warps 2-5) owns the first ceil(w/2) 8-row blocks of the item's stacked rows,
+    // group 1 (warps 12-15) the rest; each group covers all four TMEM lane quadrants.
+    SoftmaxCtx C;
+    C.p = &p;
+    C.smem = smem;
+    C.grp = warp >= 12 ? 1 : 0;
+    C.wq = warp & 3;  // TMEM lane quadrant: tokens 16 wq .. 16 wq + 15
+    C.lane = lane;
+    C.warp = warp;
+    C.tid = tid;
+    C.bar_id = C.grp ? 3 : 1;
+    C.tmem = tmem;
+    C.lane_off = uint32_t(C.wq * 32) << 16;
+    C.pt_base = smem_u32(smem + kOffPT);
+    C.c = p.scale_log2;
+    C.s_full = s_full;
+    C.pv_done = pv_done;
+    C.vfull = vfull;
+    C.p_full_g = p_full + 2 * C.grp;
+    C.o_free = o_free;
+    C.ml_full = ml_full;
+    C.xml = xml;
+    C.red_g = red + C.grp * kRedFloats;
+    C.alpha_s = reinterpret_cast<float *>(smem + kOffAlpha) + (C.grp * 4 + C.wq) * 64;
     uint32_t n = 0;
-    int it = ring_item(it_full, recs, 0);
-    if (it >= 0) {
-      Item x0;
-      decode_item(recs, x0);
-      stage_q_tmem(x0, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, wq, lane, kColQ);
-      mbar_arrive(q_full);
-    }
-    for (uint32_t item_idx = 0; it >= 0; ++item_idx) {
+    for (uint32_t item_idx = 0;; ++item_idx) {
+      const int it = ring_item(it_full, recs, item_idx);
+      if (it < 0) {
+        ring_release(it_empty, item_idx, lane);
+        break;
+      }
       const ItemRec *rec = recs + item_idx % kItemRing;
       Item x;
       decode_item(rec, x);
-      const int R8 = 8 * x.w;
-      const int rep = x.rep;
-      // M-row of this thread; M = 64 rows are shared by lane pairs (t, t + 16), half h
-      const int m64 = x.m64;
-      const int mrow = m64 ? wq * 16 + (lane & 15) : wq * 32 + lane;
-      const int h = m64 ? lane >> 4 : 0;
-      const int rpc = (m64 ? 64 : 128) / rep, cw = 64 / rep;
-      const int copy = mrow / rpc;
-      const int i = mrow - copy * rpc;  // stacked row (dead if >= R8)
-      const int colbase = copy * cw;
-      const int tw = m64 ? cw / 2 : cw;  // tokens handled by this thread
-      const int tok0 = colbase + h * tw;
-      const uint32_t ob = item_idx & 1;
-      const uint32_t tO = tmem + lane_off + kColO + ob * 128;
-      float m_run = -INFINITY, l_run = 0.f;
-      bool staged = false;  // next item's Q staged in TMEM (or there is no next item)
-      int next = -1;
-      for (int t = 0; t < x.nt; ++t) {
-        const uint32_t sb = n & 1;
-        const int2 tr = tile_rows(rec, t);  // {valid tokens, owning branch or -1}
-        const bool live = i < R8 && (tr.y < 0 || (i >> 3) == tr.y);
-        const int nvalid = live ? max(0, min(tw, tr.x - tok0)) : 0;
-        mbar_wait(s_full + sb, (n >> 1) & 1);
-        if (warp == 2 && lane == 0) trace_ev(p, 7, n);
-        tc_fence_after();
-        // P[sb] aliases S[sb]: PV(n-2) finished reading it before QK(n) was issued.
-        const uint32_t tS = tmem + lane_off + kColS + sb * 64;
-        uint64_t *pv_prev = pv_done + ((n - 1) & 1);
-        const uint32_t pv_par = ((n - 1) >> 1) & 1;
-        const bool o_live = t > 0;
-        if (m64) {
-          if (cw == 16)
-            softmax_tile<8, true>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
-          else if (cw == 32)
-            softmax_tile<16, true>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
-          else
-            softmax_tile<32, true>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
-        } else {
-          if (cw == 16)
-            softmax_tile<16, false>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
-          else if (cw == 32)
-            softmax_tile<32, false>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
-          else
-            softmax_tile<64, false>(tS, colbase, nvalid, o_live, c_log2, m_run, l_run, tO, pv_prev, pv_par);
-        }
-        tc_fence_before();
-        if (lane == 0) trace_ev(p, warp == 2 ? 8 : 6 + warp, n);  // warps 3,4,5 -> 9,10,11
-        mbar_arrive(p_full + sb);
-        ++n;
-        // Stage the next item's queries into the other Q buffer as soon as the item is
-        // claimed and its rows have landed in SMEM (never blocks here).  Q[(k+1) & 1] was
-        // last read by item k-1's QK MMAs, complete since this item's first s_full.
-        if (!staged) {
-          const uint32_t slot = (item_idx + 1) % kItemRing;
-          int ready = lane == 0 ? mbar_try_wait(it_full + slot, ((item_idx + 1) / kItemRing) & 1) : 0;
-          ready = __shfl_sync(0xffffffffu, ready, 0);
-          if (ready) {
-            next = ring_item(it_full, recs, item_idx + 1);
-            if (next < 0) {
-              staged = true;
-            } else {
-              int qready = lane == 0 ? mbar_try_wait(qs_full, qs_pass & 1) : 0;
-              qready = __shfl_sync(0xffffffffu, qready, 0);
-              if (qready) {
-                Item xn;
-                decode_item(recs + (item_idx + 1) % kItemRing, xn);
-                stage_q_tmem(xn, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, wq,
-                             lane, kColQ + ((item_idx + 1) & 1) * 64);
-                mbar_arrive(q_full);
-                staged = true;
-              }
-            }
-          }
-        }
-      }
-      if (m64) l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);  // row sum of the lane pair
-      if (!staged) {  // not staged during the item: wait for it now
-        next = ring_item(it_full, recs, item_idx + 1);
-        if (next >= 0) {
-          Item xn;
-          decode_item(recs + (item_idx + 1) % kItemRing, xn);
-          stage_q_tmem(xn, smem + kOffQS, qs_full, qs_free, qs_pass, tmem, lane_off, wq, lane,
-                       kColQ + ((item_idx + 1) & 1) * 64);
-          mbar_arrive(q_full);
-        }
+      const int wb0 = (x.w + 1) >> 1;
+      const int wb = C.grp ? x.w - wb0 : wb0;   // 8-row blocks of this group
+      const int blk0 = C.grp ? wb0 : 0;
+      switch (wb) {
+        case 0: softmax_item<0>(C, rec, x, blk0, item_idx, n); break;
+        case 1: softmax_item<1>(C, rec, x, blk0, item_idx, n); break;
+        case 2: softmax_item<2>(C, rec, x, blk0, item_idx, n); break;
+        case 3: softmax_item<3>(C, rec, x, blk0, item_idx, n); break;
+        default: softmax_item<4>(C, rec, x, blk0, item_idx, n); break;
       }
       ring_release(it_empty, item_idx, lane);
-      // publish (m, l) for the epilogue warps; xml[ob] was consumed by epilogue item_idx-2
-      mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);
-      if (h == 0) xml[ob * 128 + mrow] = make_float2(m_run, l_run);
-      mbar_arrive(ml_full + ob);
-      it = next;
     }
   } else {
     // ======================= epilogue (128 threads, warps 6-9) =======================
-    // Merges the replicated copies of each stacked row and writes the normalised partial
-    // (o, lse), overlapping the next item's tiles (O is double-buffered in TMEM).
+    // O^T[d][16 b + e (hi) / 16 b + 8 + e (lo)] -> partial row (branch b, GQA row e):
+    // thread = d, so every row is written by 128 consecutive threads (coalesced), while the
+    // next item's tiles run (O^T is double-buffered in TMEM).
     const int wq = warp & 3;
     const uint32_t lane_off = uint32_t(wq * 32) << 16;
+    const int d = wq * 32 + lane;
+    const int etid = tid - 192;  // 0..127
     for (uint32_t item_idx = 0;; ++item_idx) {
       const int it = ring_item(it_full, recs, item_idx);
       Item x;
       decode_item(recs + item_idx % kItemRing, x);
       ring_release(it_empty, item_idx, lane);
       if (it < 0) break;
-      const int R8 = 8 * x.w;
-      const int rep = x.rep;
-      const int mrow = mrow_of(x.m64, wq, lane);
-      const int rpc = (x.m64 ? 64 : 128) / rep;
-      const int copy = mrow >= 0 ? mrow / rpc : 0;
-      const int i = mrow >= 0 ? mrow - copy * rpc : 1 << 20;
       const uint32_t ob = item_idx & 1;
       const uint32_t tO = tmem + lane_off + kColO + ob * 128;
       mbar_wait(ml_full + ob, (item_idx >> 1) & 1);
       mbar_wait(o_full + ob, (item_idx >> 1) & 1);
       if (warp == 6 && lane == 0) trace_ev(p, 10, 2048 + item_idx);
+      if (p.trace != nullptr && blockIdx.x == 0 && warp == 6 && lane == 0 &&
+          2048 + int(item_idx) < p.trace_cap) {
+        long long *tr = p.trace + (size_t)(2048 + item_idx) * 16;
+        tr[13] = x.w; tr[14] = x.nt; tr[15] = x.local;
+      }
       tc_fence_after();
-      const bool has = mrow >= 0 && i < R8;
-      const float2 mine = has ? xml[ob * 128 + mrow] : make_float2(-INFINITY, 0.f);
-      float M = -INFINITY, L = 0.f;
-      if (has) {
-        for (int c = 0; c < rep; ++c) M = fmaxf(M, xml[ob * 128 + c * rpc + i].x);
-        for (int c = 0; c < rep; ++c) {
-          const float2 ml = xml[ob * 128 + c * rpc + i];
-          if (ml.y > 0.f) L += ex2(ml.x - M) * ml.y;
-        }
-      }
-      const float f = (L > 0.f && mine.y > 0.f) ? ex2(mine.x - M) / L : 0.f;
-      if (warp == 6 && lane == 0) trace_ev(p, 12, 2048 + item_idx);
-      const bool out_row = has;
-      const bool warp_out = __any_sync(0xffffffffu, out_row);
-      const int etid = tid - 192;  // 0..127
-      if (out_row && copy == 0) {
-        const size_t prow = ((size_t)(x.cs0 + (i >> 3)) * h + x.g) * kGroup + (i & 7);
-        p.part_lse[prow] = L > 0.f ? (M + __log2f(L)) * 0.69314718055994531f : -INFINITY;
-      }
-      // 16-column passes: every copy stages its scaled O row slice in SMEM, then all 128
-      // threads sum the copies and write the rows with coalesced stores
-      constexpr int kF4 = kXCols / 4;  // float4 per row slice
 #pragma unroll 1
-      for (int pass = 0; pass < kHeadDim / kXCols; ++pass) {
-        if (warp_out) {
-          uint32_t o[16];
-          tmem_ld16(tO + pass * kXCols, o);
-          tmem_ld_wait();
-          if (out_row) {
-            float4 *xr = reinterpret_cast<float4 *>(xo + mrow * kXStride);
+      for (int b = 0; b < x.w; ++b) {
+        uint32_t o[16];
+        tmem_ld16(tO + 16 * b, o);
+        tmem_ld_wait();
+        const size_t prow0 = ((size_t)(x.cs0 + b) * h + x.g) * kGroup;
 #pragma unroll
-            for (int j = 0; j < kF4; ++j)
-              xr[j] = make_float4(__uint_as_float(o[4 * j]) * f, __uint_as_float(o[4 * j + 1]) * f,
-                                  __uint_as_float(o[4 * j + 2]) * f,
-                                  __uint_as_float(o[4 * j + 3]) * f);
-          }
+        for (int e = 0; e < 8; ++e) {
+          const float2 ml = xml[ob * 64 + 8 * b + e];
+          const float inv = ml.y > 0.f ? 1.f / ml.y : 0.f;
+          p.part_o[(prow0 + e) * kHeadDim + d] = (__uint_as_float(o[e]) + __uint_as_float(o[8 + e])) * inv;
         }
-        named_bar_sync(2, 128);
-        for (int k = etid; k < R8 * kF4; k += 128) {
-          const int row = k / kF4, c4 = k % kF4;
-          float4 a = reinterpret_cast<const float4 *>(xo + row * kXStride)[c4];
-          for (int cc = 1; cc < rep; ++cc) {
-            const float4 b = reinterpret_cast<const float4 *>(xo + (cc * rpc + row) * kXStride)[c4];
-            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-          }
-          const size_t prow = ((size_t)(x.cs0 + (row >> 3)) * h + x.g) * kGroup + (row & 7);
-          reinterpret_cast<float4 *>(p.part_o + prow * kHeadDim + pass * kXCols)[c4] = a;
+        if (etid < 8) {
+          const float2 ml = xml[ob * 64 + 8 * b + etid];
+          p.part_lse[prow0 + etid] =
+              ml.y > 0.f ? (ml.x + __log2f(ml.y)) * 0.69314718055994531f : -INFINITY;
         }
-        named_bar_sync(2, 128);  // staging reused by the next pass / item
       }
       // publish: this item's partials of (request, KV head) are complete (release)
       __threadfence();
       named_bar_sync(2, 128);
       if (etid == 0) atomicAdd(p.done + x.r * kGroup + x.g, 1);
-      if (warp == 6 && lane == 0) trace_ev(p, 14, 2048 + item_idx);
-      if (warp == 8 && lane == 0) trace_ev(p, 15, 2048 + item_idx);
-      tc_fence_before();
       if (warp == 6 && lane == 0) trace_ev(p, 11, 2048 + item_idx);
+      tc_fence_before();
       mbar_arrive(o_free + ob);
     }
   }
@@ -868,15 +934,17 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) 
   const int n_adm = __ldg(p.hdr + 2);
   const int qheads = kGroup * h;
   for (int k = blockIdx.x; k < n_adm; k += gridDim.x) {
-    const int4 md = __ldg(p.merge_desc + k);  // {slot, first chunk-slot, partials, width | r << 16}
-    const int s = md.x, nq = md.z, w = md.w & 0xffff, r = md.w >> 16;
+    // {slot, first shared partial, prefix chunks, width}, {first local partial, local items,
+    // request, items of the request per KV head}
+    const int4 md = __ldg(p.merge_desc + 2 * k);
+    const int4 ml = __ldg(p.merge_desc + 2 * k + 1);
+    const int s = md.x, nc = md.z, w = md.w, r = ml.z;
+    const int nq = nc + ml.y, target = ml.w;
     for (int g = warp; g < h; g += kMergeThreads / 32) {
-      const size_t row0 = ((size_t)md.y * h + g) * kGroup;
-      const size_t qstride = (size_t)w * h * kGroup;  // partial rows between items
       int32_t *cnt = p.done + r * kGroup + g;
-      if (ld_acquire(cnt) < nq) {  // bounded spin: a lost publication traps, never hangs
+      if (ld_acquire(cnt) < target) {  // bounded spin: a lost publication traps, never hangs
         const long long t0 = clock64();
-        while (ld_acquire(cnt) < nq) {
+        while (ld_acquire(cnt) < target) {
           __nanosleep(256);
           if (clock64() - t0 > (1ll << 35)) __trap();
         }
@@ -893,7 +961,9 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) 
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const bool ok = q0 + u < nq;
-          const size_t prow = row0 + (size_t)(q0 + u) * qstride;
+          const int q = q0 + u;  // prefix chunk q (stride w), then the slot's own local items
+          const size_t cs = q < nc ? (size_t)md.y + (size_t)q * w : (size_t)ml.x + (q - nc);
+          const size_t prow = (cs * h + g) * kGroup;
           if (ok && (lane >> 3) == u) l2 = __ldcg(p.part_lse + prow + (lane & 7)) * 1.4426950408889634f;
 #pragma unroll
           for (int a = 0; a < kGroup; ++a)
@@ -967,7 +1037,7 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-static int make_kv_map(CUtensorMap *map, const void *pool, const taper_kv *kv) {
+static int make_kv_map(CUtensorMap *map, const void *pool, const taper_kv *kv, bool box16 = false) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return fail(TAPER_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t row = 128 * 2;
@@ -978,7 +1048,8 @@ static int make_kv_map(CUtensorMap *map, const void *pool, const taper_kv *kv) {
     // the [d-half][token][64] layout of two SW128 K-major atoms
     cuuint64_t dims[5] = {64, ps, 2, hl, (cuuint64_t)kv->num_pages};
     cuuint64_t strides[4] = {row, 128, row * ps, row * ps * hl};
-    cuuint32_t box[5] = {64, (cuuint32_t)kTile, 2, 1, 1};
+    // box16: {64 d, 16 tokens, one d-half} for the partial last tile of a segment
+    cuuint32_t box[5] = {64, box16 ? 16u : (cuuint32_t)kTile, box16 ? 1u : 2u, 1, 1};
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(pool), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -993,6 +1064,23 @@ static int make_kv_map(CUtensorMap *map, const void *pool, const taper_kv *kv) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   if (r != CUDA_SUCCESS) return fail(TAPER_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return TAPER_OK;
+}
+
+// q [S][8 h][128] bf16 viewed as (d-lo 64, GQA row 8, d-half 2, slot * h + g): one
+// {64, 8, 2, 1} box = the 8 rows of one (slot, KV head) as [d-half][8][128 B] with SW128,
+// the K-major B-operand layout of Q^T.
+static int make_q_map(CUtensorMap *map, const void *q, int S, int h) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return fail(TAPER_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {64, (cuuint64_t)kGroup, 2, (cuuint64_t)S * (cuuint64_t)h};
+  cuuint64_t strides[3] = {256, 128, 256 * kGroup};
+  cuuint32_t box[4] = {64, (cuuint32_t)kGroup, 2, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(q), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TAPER_ERR_CUDA, "cuTensorMapEncodeTiled (q) failed");
   return TAPER_OK;
 }
 
@@ -1049,10 +1137,12 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   char *w = static_cast<char *>(workspace);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
-  CUtensorMap tmK, tmV;
+  CUtensorMap tmK, tmV, tmK16, tmV16, tmQ;
   int rc = make_kv_map(&tmK, kv->k_pages, kv);
-  if (rc != TAPER_OK) return rc;
-  rc = make_kv_map(&tmV, kv->v_pages, kv);
+  if (rc == TAPER_OK) rc = make_kv_map(&tmV, kv->v_pages, kv);
+  if (rc == TAPER_OK) rc = make_kv_map(&tmK16, kv->k_pages, kv, kv->page_size >= kTile);
+  if (rc == TAPER_OK) rc = make_kv_map(&tmV16, kv->v_pages, kv, kv->page_size >= kTile);
+  if (rc == TAPER_OK) rc = make_q_map(&tmQ, q, S, kv->h_local);
   if (rc != TAPER_OK) return rc;
 
   static thread_local bool attr_set = false;
@@ -1073,7 +1163,6 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   ap.adm_by_req = reinterpret_cast<const int32_t *>(w + L.adm_by_req);
   ap.items = reinterpret_cast<const ItemDesc *>(w + tabs.items);
   ap.ltiles = reinterpret_cast<const int4 *>(w + tabs.ltiles);
-  ap.q = static_cast<const __nv_bfloat16 *>(q);
   ap.part_lse = reinterpret_cast<float *>(w + tabs.lse);
   ap.part_o = reinterpret_cast<float *>(w + tabs.o);
   ap.h_local = h;
@@ -1096,7 +1185,7 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   cfg.stream = st;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, attend_kernel, tmK, tmV, ap);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attend_kernel, tmK, tmV, tmK16, tmV16, tmQ, ap);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail_cuda(e, "attend_kernel launch");
   if (g_prof_ev[1]) cudaEventRecord(g_prof_ev[1], st);

@@ -16,6 +16,7 @@ constexpr int kChunk = TAPER_CHUNK_TOKENS;
 constexpr int kMaxSlots = TAPER_MAX_SLOTS;
 constexpr int kTileTokens = 64;       // tokens per pipeline tile (one TMA stage)
 constexpr int kLocalItemTiles = 16;   // branch-local tiles per local work item
+constexpr int kMaxItemBranches = 8;   // admitted branches stacked in one shared item (N <= 64)
 
 // ------------------------------------------------------------------ workspace layout
 // hdr[0] = n_rc    : number of (request, prefix chunk) pairs (shared items per KV head)
@@ -44,7 +45,7 @@ __host__ __device__ inline WsLayout ws_layout(int R, int S) {
   w.req_part_off = o;  o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
   w.req_adm_off = o;   o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
   w.adm_by_req = o;    o = ws_align(o + size_t(S) * sizeof(int32_t));
-  w.merge_desc = o;    o = ws_align(o + size_t(S) * 4 * sizeof(int32_t));
+  w.merge_desc = o;    o = ws_align(o + size_t(S) * 8 * sizeof(int32_t));
   // per (request, KV head): [0, R*8) items whose partials are written (attend -> merge),
   // [R*8, 2*R*8) merge warps done reading them (the last one re-arms both)
   w.done = o;          o = ws_align(o + size_t(R) * 2 * kGroup * sizeof(int32_t));
@@ -129,10 +130,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a lost arrival traps (error 700-class) instead of hanging the GPU.
+// Bounded wait: a lost arrival traps (error 700-class) instead of hanging the GPU.  The
+// clock read between polls doubles as a short backoff: a tight try_wait loop (measured)
+// slows the kernel ~5 %, the polls competing with the SMEM traffic of the busy warps.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
-  long long t0 = clock64();
+  const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
     if (clock64() - t0 > (1ll << 35)) __trap();  // ~17 s at 2 GHz
   }

@@ -1,5 +1,6 @@
 """Dev tool (GPU box): same-box A/B of library variants built with different -D defines.
-    python scripts/ab.py NAME=DEF1,DEF2 NAME2= ...   (empty define list = baseline)
+    python scripts/ab.py NAME=DEF1,DEF2 NAME2= NAME3=@path/lib.so ...
+(empty define list = the working tree as is; @path = a prebuilt library)
 Builds /tmp/libtaper_<NAME>.so per variant, then alternates scripts/layer_time.py runs."""
 import os
 import subprocess
@@ -12,6 +13,9 @@ from paper_2605_06914_b200 import build as B  # noqa: E402
 variants = []
 for a in sys.argv[1:]:
     name, _, defs = a.partition("=")
+    if defs.startswith("@"):  # prebuilt library
+        variants.append((name, os.path.join(ROOT, defs[1:])))
+        continue
     lib = f"/tmp/libtaper_{name}.so"
     B.build(force=True, defines=[d for d in defs.split(",") if d], out=lib)
     variants.append((name, lib))

@@ -53,6 +53,7 @@ def main():
         (cta[:, 0].min() - g0) / 1e3, (cta[:, 0].max() - g0) / 1e3, np.median(cta[:, 2] - g0) / 1e3,
         (cta[:, 1].min() - g0) / 1e3, np.median(cta[:, 1] - g0) / 1e3, (cta[:, 1].max() - g0) / 1e3))
     a = tr.view(cap, 16).cpu().numpy()
+    np.save("gpurun_out/trace_raw.npy", a)
     n = int((a[:, 1] > 0).sum())
     a = a[:n].astype(np.int64)
     t0 = a[0, 0]
