@@ -47,8 +47,10 @@ constexpr int kOffQ = kOffV + kVStages * kStageBytes;   // Q^T operand, 2 buffer
 constexpr int kQBytes = kMaxItemBranches * kGroup * 256;  // 16 KB: [branch][d-half][8][128 B]
 constexpr int kOffPT = kOffQ + 2 * kQBytes;              // P^T operand: 128 rows x 128 B
 constexpr int kPTBytes = 2 * kMaxItemBranches * kGroup * 128;
-constexpr int kPTBufs = 1;  // a second buffer (decoupling PV(n-1) from softmax(n)) measured no gain
-constexpr int kOffML = kOffPT + kPTBufs * kPTBytes;  // (m, l) of the 64 stacked rows, 2 buffers
+// Items with <= 4 branches (P^T <= 8 KB) alternate between the two 8 KB halves by tile
+// parity, so softmax(n) only waits for PV(n-2); wider items use the whole buffer.
+constexpr int kNarrowPT = 4;
+constexpr int kOffML = kOffPT + kPTBytes;  // (m, l) of the 64 stacked rows, 2 buffers
 // cross-warp reductions per softmax group: max [2 parities][4 warps][64], sum [4][64]
 constexpr int kRedFloats = 3 * 4 * 64;
 constexpr int kOffRed = kOffML + 2 * 64 * 8;
@@ -218,6 +220,20 @@ __device__ __forceinline__ void stmatrix_x4_trans(uint32_t addr, uint32_t r0, ui
                : "memory");
 }
 
+// bar.red.or over a named barrier: true iff any of the n participating threads passes true
+__device__ __forceinline__ bool bar_red_or(int id, int n_threads, bool pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, %2, %3, p;\n\t"
+      "selp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"(uint32_t(pred)), "r"(id), "r"(n_threads)
+      : "memory");
+  return r != 0;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t *>(&h2);
@@ -254,7 +270,8 @@ struct SoftmaxCtx {  // per-thread constants of a softmax warp
 // WB = 0: the group has no rows in this item and only keeps the barrier phases in step.
 template <int WB>
 __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec *rec, const Item &x,
-                                             int blk0, uint32_t item_idx, uint32_t &n) {
+                                             int blk0, uint32_t item_idx, uint32_t &n,
+                                             bool &prev_wide) {
   constexpr int NC = WB > 0 ? 2 * WB : 2;    // columns per thread
   constexpr int NF = bfly_cnt(NC, 3);        // columns a lane owns after the butterfly
   const int lane = C.lane, wq = C.wq;
@@ -284,6 +301,7 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
     }
   }
   const bool rows_live = 8 * (blk0 + WB) <= n_live;
+  const bool wide = x.w > kNarrowPT;
   float m_run[NC], l_run[NC], m_red[NF];
 #pragma unroll
   for (int i = 0; i < NC; ++i) { m_run[i] = -INFINITY; l_run[i] = 0.f; }
@@ -302,6 +320,7 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
       uint32_t s[4 * WB];
       tmem_ld_16x256<WB>(tS + 8 * blk0, s);
       tmem_ld_wait();
+      if (C.warp == 2 && lane == 0) trace_ev(*C.p, 4, n);
       float x2[4 * WB];
 #pragma unroll
       for (int i = 0; i < 4 * WB; ++i) x2[i] = __uint_as_float(s[i]);
@@ -316,54 +335,68 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
             if (!(live && vB)) x2[4 * b + 2 + e] = -INFINITY;
           }
       }
+      // Lazy max: the running maxima only move when some score exceeds them by > 8 (log2
+      // units).  One barrier-reduction tells the group whether any thread sees such a
+      // score; only then is the exact column max reduced (butterfly + SMEM exchange).
       float v[NC];
+      bool exceed = false;
 #pragma unroll
-      for (int i = 0; i < NC; ++i) v[i] = fmaxf(x2[4 * (i >> 1) + (i & 1)], x2[4 * (i >> 1) + 2 + (i & 1)]);
+      for (int i = 0; i < NC; ++i) {
+        v[i] = fmaxf(x2[4 * (i >> 1) + (i & 1)], x2[4 * (i >> 1) + 2 + (i & 1)]);
+        exceed |= v[i] * C.c > m_run[i] + 8.f;
+      }
+      if (bar_red_or(C.bar_id, 128, exceed)) {
 #pragma unroll
-      for (int st = 0; st < 3; ++st) {
-        const int M = 16 >> st;
-        const int cnt = bfly_cnt(NC, st);
-        if (cnt % 2 == 0) {
-          const bool up = (lane & M) != 0;
+        for (int st = 0; st < 3; ++st) {
+          const int M = 16 >> st;
+          const int cnt = bfly_cnt(NC, st);
+          if (cnt % 2 == 0) {
+            const bool up = (lane & M) != 0;
 #pragma unroll
-          for (int j = 0; j < cnt / 2; ++j) {
-            const float send = up ? v[j] : v[cnt / 2 + j];
-            const float keep = up ? v[cnt / 2 + j] : v[j];
-            v[j] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, M));
+            for (int j = 0; j < cnt / 2; ++j) {
+              const float send = up ? v[j] : v[cnt / 2 + j];
+              const float keep = up ? v[cnt / 2 + j] : v[j];
+              v[j] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, M));
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < cnt; ++j) v[j] = fmaxf(v[j], __shfl_xor_sync(0xffffffffu, v[j], M));
           }
-        } else {
-#pragma unroll
-          for (int j = 0; j < cnt; ++j) v[j] = fmaxf(v[j], __shfl_xor_sync(0xffffffffu, v[j], M));
         }
-      }
 #pragma unroll
-      for (int j = 0; j < NF; ++j) red_max[wq * 64 + col[j]] = v[j];
-      named_bar_sync(C.bar_id, 128);
+        for (int j = 0; j < NF; ++j) red_max[wq * 64 + col[j]] = v[j];
+        named_bar_sync(C.bar_id, 128);
+        if (C.warp == 2 && lane == 0) trace_ev(*C.p, 13, n);
 #pragma unroll
-      for (int j = 0; j < NF; ++j) {
-        float mx = fmaxf(fmaxf(red_max[col[j]], red_max[64 + col[j]]),
-                         fmaxf(red_max[128 + col[j]], red_max[192 + col[j]]));
-        mx *= C.c;  // log2 units (c = softmax scale * log2 e > 0)
-        if (mx > m_red[j] + 8.f) m_red[j] = mx;
-        v[j] = m_red[j];
-      }
+        for (int j = 0; j < NF; ++j) {
+          float mx = fmaxf(fmaxf(red_max[col[j]], red_max[64 + col[j]]),
+                           fmaxf(red_max[128 + col[j]], red_max[192 + col[j]]));
+          mx *= C.c;  // log2 units (c = softmax scale * log2 e > 0)
+          if (mx > m_red[j] + 8.f) m_red[j] = mx;
+          v[j] = m_red[j];
+        }
 #pragma unroll
-      for (int st = 2; st >= 0; --st) {
-        const int M = 16 >> st;
-        const int cnt = bfly_cnt(NC, st);
-        if (cnt % 2 == 0) {
-          const bool up = (lane & M) != 0;
-          float lo[NC], hi[NC];
+        for (int st = 2; st >= 0; --st) {
+          const int M = 16 >> st;
+          const int cnt = bfly_cnt(NC, st);
+          if (cnt % 2 == 0) {
+            const bool up = (lane & M) != 0;
+            float lo[NC], hi[NC];
 #pragma unroll
-          for (int j = 0; j < cnt / 2; ++j) {
-            const float recv = __shfl_xor_sync(0xffffffffu, v[j], M);
-            lo[j] = up ? recv : v[j];
-            hi[j] = up ? v[j] : recv;
+            for (int j = 0; j < cnt / 2; ++j) {
+              const float recv = __shfl_xor_sync(0xffffffffu, v[j], M);
+              lo[j] = up ? recv : v[j];
+              hi[j] = up ? v[j] : recv;
+            }
+#pragma unroll
+            for (int j = 0; j < cnt / 2; ++j) { v[j] = lo[j]; v[cnt / 2 + j] = hi[j]; }
           }
-#pragma unroll
-          for (int j = 0; j < cnt / 2; ++j) { v[j] = lo[j]; v[cnt / 2 + j] = hi[j]; }
         }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NC; ++i) v[i] = m_run[i];
       }
+      if (C.warp == 2 && lane == 0) trace_ev(*C.p, 9, n);
       bool need_any = false;
       float alpha[NC];
 #pragma unroll
@@ -397,10 +430,11 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
         pk[4 * b + 2] = pack_bf16(pA[0] - fA.x, pA[1] - fA.y);
         pk[4 * b + 3] = pack_bf16(pB[0] - fB.x, pB[1] - fB.y);
       }
-      // the P^T buffer this tile writes was last read by PV(n - kPTBufs); an O rescale
-      // needs PV(n-1) complete
+      if (C.warp == 2 && lane == 0) trace_ev(*C.p, 10, n);
+      // the P^T (half) buffer this tile writes was last read by PV(n-2) when this and the
+      // previous tile are narrow, else by PV(n-1); an O rescale needs PV(n-1) complete
       const bool rescale = t > 0 && __any_sync(0xffffffffu, need_any);
-      if ((rescale || kPTBufs == 1) && n >= 1)
+      if ((rescale || wide || prev_wide) && n >= 1)
         mbar_wait(C.pv_done + ((n - 1) & 1), ((n - 1) >> 1) & 1);
       else if (n >= 2)
         mbar_wait(C.pv_done + (n & 1), ((n - 2) >> 1) & 1);
@@ -428,13 +462,16 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
         }
         tmem_st_wait();
       }
-      const uint32_t pbuf = (n % kPTBufs) * kPTBytes;
+      if (C.warp == 2 && lane == 0) trace_ev(*C.p, 14, n);
+      const uint32_t pbuf = wide ? 0u : (n & 1) * (kPTBytes / 2);
 #pragma unroll
       for (int b = 0; b < WB; ++b)
         stmatrix_x4_trans(st_addr[b] + pbuf, pk[4 * b], pk[4 * b + 1], pk[4 * b + 2], pk[4 * b + 3]);
-    } else if (n >= uint32_t(kPTBufs)) {  // no rows: keep in step with the writers
-      mbar_wait(C.pv_done + ((n - kPTBufs) & 1), ((n - kPTBufs) >> 1) & 1);
+      if (C.warp == 2 && lane == 0) trace_ev(*C.p, 15, n);
+    } else if (n >= 2) {  // no rows: keep in step with the writers (p_full parity phases)
+      mbar_wait(C.pv_done + (n & 1), ((n - 2) >> 1) & 1);
     }
+    prev_wide = wide;
     if (C.grp == 0 && nvalid < kTile) {
       // partial tile: V rows past the last valid token were not loaded (or hold tokens
       // past the sequence end); zero them so 0 * garbage cannot reach O
@@ -764,7 +801,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           mbar_wait(vfull + vs, (m / kVStages) & 1);
           tc_fence_after();
           if (elect_one()) {
-            issue_pv(tO, sV + vs * kStageBytes, sPT + (m % kPTBufs) * kPTBytes, first, idesc_pv);
+            issue_pv(tO, sV + vs * kStageBytes,
+                     sPT + (wi > kNarrowPT ? 0u : (m & 1) * (kPTBytes / 2)), first, idesc_pv);
             tc_commit(vempty + vs);
             tc_commit(pv_done + (m & 1));
             if (t == nt) tc_commit(o_full + ob);
@@ -802,6 +840,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     C.red_g = red + C.grp * kRedFloats;
     C.alpha_s = reinterpret_cast<float *>(smem + kOffAlpha) + (C.grp * 4 + C.wq) * 64;
     uint32_t n = 0;
+    bool prev_wide = true;
     for (uint32_t item_idx = 0;; ++item_idx) {
       const int it = ring_item(it_full, recs, item_idx);
       if (it < 0) {
@@ -815,11 +854,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const int wb = C.grp ? x.w - wb0 : wb0;   // 8-row blocks of this group
       const int blk0 = C.grp ? wb0 : 0;
       switch (wb) {
-        case 0: softmax_item<0>(C, rec, x, blk0, item_idx, n); break;
-        case 1: softmax_item<1>(C, rec, x, blk0, item_idx, n); break;
-        case 2: softmax_item<2>(C, rec, x, blk0, item_idx, n); break;
-        case 3: softmax_item<3>(C, rec, x, blk0, item_idx, n); break;
-        default: softmax_item<4>(C, rec, x, blk0, item_idx, n); break;
+        case 0: softmax_item<0>(C, rec, x, blk0, item_idx, n, prev_wide); break;
+        case 1: softmax_item<1>(C, rec, x, blk0, item_idx, n, prev_wide); break;
+        case 2: softmax_item<2>(C, rec, x, blk0, item_idx, n, prev_wide); break;
+        case 3: softmax_item<3>(C, rec, x, blk0, item_idx, n, prev_wide); break;
+        default: softmax_item<4>(C, rec, x, blk0, item_idx, n, prev_wide); break;
       }
       ring_release(it_empty, item_idx, lane);
     }
