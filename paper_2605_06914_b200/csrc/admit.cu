@@ -32,7 +32,7 @@ struct AdmitParams {
   int32_t *adm_list, *n_adm;
   double *diag;
   int32_t *status;
-  int32_t *hdr, *slot_req, *slot_rank, *req_chunk_off, *req_loc_off, *req_part_off,
+  int32_t *hdr, *slot_req, *slot_rank, *slot_lbase, *req_chunk_off, *req_loc_off, *req_part_off,
       *req_adm_off, *adm_by_req;
   int4 *merge_desc;  // [2 S] per admitted slot k (adm_list order): {slot, first shared
                      //     partial, prefix chunks, width}, {first local partial, local
@@ -354,10 +354,10 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
   __syncthreads();
   // item and local-tile descriptors (A5): one request per thread
   const bool fits = (long long)tot_cs <= p.cap_cs;
-#pragma unroll
-  for (int k = 0; k < kPerThread; ++k) {
-    int r = tid * kPerThread + k;
-    if (r >= R || !fits || (sh_status & TAPER_STATUS_BAD_LENGTH)) continue;
+  // (strided over the block: requests are independent here, and a latency-bound chain
+  // per thread is shorter when every thread takes at most ceil(R / 1024) requests)
+  for (int r = tid; r < R; r += blockDim.x) {
+    if (!fits || (sh_status & TAPER_STATUS_BAD_LENGTH)) continue;
     const int w = p.req_adm_off[r + 1] - p.req_adm_off[r];
     if (w == 0) continue;
     const int adm_off = p.req_adm_off[r];
@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     for (int j = 0; j < w; ++j) {
       const int s = p.adm_by_req[adm_off + j];
       const int L = p.Lloc[s];
+      p.slot_lbase[s] = li;  // local items of the request's branches before j
       for (int t0 = 0; t0 < L; t0 += kTileTokens * kLocalItemTiles, ++li) {
         const int nt = min(kLocalItemTiles, (L - t0 + kTileTokens - 1) / kTileTokens);
         for (int t = 0; t < nt; ++t) {
@@ -424,10 +425,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       const int nc = (p.req_chunk_off[r + 1] - p.req_chunk_off[r]) / groups;
       const int n_items = (p.req_chunk_off[r + 1] - p.req_chunk_off[r]) +
                           (p.req_loc_off[r + 1] - p.req_loc_off[r]);
-      int lpre = 0;  // local items of the request's branches before j
-      for (int jj = 0; jj < j; ++jj)
-        lpre += (p.Lloc[p.adm_by_req[p.req_adm_off[r] + jj]] + kTileTokens * kLocalItemTiles - 1) /
-                (kTileTokens * kLocalItemTiles);
+      const int lpre = p.slot_lbase[s];
       const int nl = (p.Lloc[s] + kTileTokens * kLocalItemTiles - 1) / (kTileTokens * kLocalItemTiles);
       const int cs_r = p.req_part_off[r];
       p.merge_desc[2 * fl[k]] = make_int4(s, cs_r + j, nc, w);
@@ -500,6 +498,7 @@ static int launch_admit(const taper_batch *batch, const taper_latency_model *mod
   p.hdr = reinterpret_cast<int32_t *>(w + L.hdr);
   p.slot_req = reinterpret_cast<int32_t *>(w + L.slot_req);
   p.slot_rank = reinterpret_cast<int32_t *>(w + L.slot_rank);
+  p.slot_lbase = reinterpret_cast<int32_t *>(w + L.slot_lbase);
   p.req_chunk_off = reinterpret_cast<int32_t *>(w + L.req_chunk_off);
   p.req_part_off = reinterpret_cast<int32_t *>(w + L.req_part_off);
   p.req_loc_off = reinterpret_cast<int32_t *>(w + L.req_loc_off);

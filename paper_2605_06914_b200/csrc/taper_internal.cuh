@@ -28,8 +28,8 @@ constexpr int kMaxItemBranches = 8;   // admitted branches stacked in one shared
 // hdr[8] = work counter of attend_kernel's dynamic scheduler (reset by admit and by the
 //          last attend CTA to exit, counted in hdr[9])
 struct WsLayout {
-  size_t hdr, slot_req, slot_rank, req_chunk_off, req_loc_off, req_part_off, req_adm_off,
-      adm_by_req, merge_desc, done, part_lse, part_o, fixed;
+  size_t hdr, slot_req, slot_rank, slot_lbase, req_chunk_off, req_loc_off, req_part_off,
+      req_adm_off, adm_by_req, merge_desc, done, part_lse, part_o, fixed;
 };
 
 __host__ __device__ inline size_t ws_align(size_t x) { return (x + 255) & ~size_t(255); }
@@ -40,6 +40,7 @@ __host__ __device__ inline WsLayout ws_layout(int R, int S) {
   w.hdr = o;           o = ws_align(o + 16 * sizeof(int32_t));
   w.slot_req = o;      o = ws_align(o + size_t(S) * sizeof(int32_t));
   w.slot_rank = o;     o = ws_align(o + size_t(S) * sizeof(int32_t));
+  w.slot_lbase = o;    o = ws_align(o + size_t(S) * sizeof(int32_t));  // first local item of r
   w.req_chunk_off = o; o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
   w.req_loc_off = o;   o = ws_align(o + size_t(R + 1) * sizeof(int32_t));
   w.req_part_off = o;  o = ws_align(o + size_t(R + 1) * sizeof(int32_t));

@@ -128,3 +128,36 @@ def test_partial_admission_outputs(policy):
     n = int(adm.n_adm.item())
     assert b.n_req <= n < b.n_slot
     _check_all(case, adm, out, lse, heads=[0, 9, 63], what=policy)
+
+
+@pytest.mark.parametrize("page", [16, 64])
+def test_garbage_past_sequence_end(page):
+    """Token slots of the pool past every segment's end (the tail of its last page, spare
+    pages) hold NaN: a partial tile must never let them reach O (P = 0 there, but
+    0 * NaN = NaN), and the result must still match the oracle, which reads valid tokens
+    only."""
+    rng = np.random.default_rng(5)
+    lsh = [100, 1, 64, 1000, 65, 2049]
+    fan = [3, 1, 2, 5, 1, 8]
+    loc = rng.integers(1, 140, size=sum(fan)).tolist()
+    b = synth.make_batch(lsh, fan, loc, 1e3, 0.0, rng=rng)
+    case = Case(b, page=page, seed=9)
+    lay = case.layout
+    valid = np.zeros((lay.num_pages, page), bool)
+
+    def mark(pages, n_tok):
+        for j, pg in enumerate(pages):
+            valid[pg, : max(0, min(page, n_tok - j * page))] = True
+
+    for r in range(b.n_req):
+        mark(lay.req_pages[lay.req_page_off[r]:lay.req_page_off[r + 1]], int(b.req_shared_len[r]))
+    for s in range(b.n_slot):
+        mark(lay.slot_pages[lay.slot_page_off[s]:lay.slot_page_off[s + 1]], int(b.slot_local_len[s]))
+    bad = torch.from_numpy(~valid)
+    assert bad.any()
+    case.k[bad.nonzero(as_tuple=True)[0], :, bad.nonzero(as_tuple=True)[1]] = float("nan")
+    case.v[bad.nonzero(as_tuple=True)[0], :, bad.nonzero(as_tuple=True)[1]] = float("nan")
+    adm, out, lse = case.run_gpu(policy="eager")
+    adm_slots = np.flatnonzero(adm.slot_admitted.cpu().numpy()[:b.n_slot])
+    assert torch.isfinite(out[adm_slots]).all()
+    _check_all(case, adm, out, lse, what=f"nan tail page={page}")
