@@ -42,6 +42,7 @@ struct AdmitParams {
   int h_local;
   ItemDesc *items;   // [cap_cs] work items (A5)
   int4 *ltiles;      // [cap_cs * 16] local tiles {slot, tok0, valid, jrow}
+  int32_t *order;    // [cap_cs] claim order of the items (longest first)
 };
 
 __device__ __forceinline__ double T_eval(double a, double b, double c, long long n,
@@ -432,6 +433,31 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       p.merge_desc[2 * fl[k] + 1] = make_int4(cs_r + nc * w + lpre, nl, r, n_items);
     }
   }
+  // claim order (longest processing time first): the dynamic scheduler of attend_kernel
+  // hands out items in this order, so the last claims are the shortest and the CTAs finish
+  // together.  Cost ~ tiles x (2, or 3 for > 4 stacked branches: their softmax is ~1.4x a
+  // narrow tile's); ties keep request-major order.  More than 4096 items: as emitted.
+  {
+    const int D = ((long long)tot_cs <= p.cap_cs && !(sh_status & TAPER_STATUS_BAD_LENGTH)) ? tot_nc + tot_nl : 0;
+    if (D <= kMaxSlots) {
+      int n_keys = 1;
+      while (n_keys < D) n_keys <<= 1;
+      for (int i = tid; i < n_keys; i += blockDim.x) {
+        unsigned long long key = ~0ull;
+        if (i < D) {
+          const ItemDesc d = p.items[i];
+          const int cost = d.nt * (d.w > 4 ? 3 : 2);
+          key = ((unsigned long long)(0xffff - cost) << 32) | (unsigned)i;
+        }
+        keys[i] = key;
+      }
+      __syncthreads();
+      bitonic_sort(keys, n_keys);
+      for (int i = tid; i < D; i += blockDim.x) p.order[i] = int(keys[i] & 0xffffffffu);
+    } else {
+      for (int i = tid; i < D; i += blockDim.x) p.order[i] = i;
+    }
+  }
   if (tid == 0) {
     int st = sh_status;
     int n_rc = tot_nc, n_rl = tot_nl;
@@ -510,6 +536,7 @@ static int launch_admit(const taper_batch *batch, const taper_latency_model *mod
   p.cap_cs = T.cap_cs;
   p.items = reinterpret_cast<ItemDesc *>(w + T.items);
   p.ltiles = reinterpret_cast<int4 *>(w + T.ltiles);
+  p.order = reinterpret_cast<int32_t *>(w + T.order);
   p.h_local = h_local;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (S > 0) {
