@@ -473,14 +473,14 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
       mbar_wait(C.pv_done + (n & 1), ((n - 2) >> 1) & 1);
     }
     prev_wide = wide;
-    if (C.grp == 0 && nvalid < kTile) {
+    if (C.grp == 1 && nvalid < kTile) {  // group 1 has fewer (w = 1: no) rows
       // partial tile: V rows past the last valid token were not loaded (or hold tokens
       // past the sequence end); zero them so 0 * garbage cannot reach O
       const uint32_t vs = n % kVStages;
       mbar_wait(C.vfull + vs, (n / kVStages) & 1);
       uint8_t *vt = C.smem + kOffV + vs * kStageBytes;
       const int nz = (kTile - nvalid) * 8;  // 16 B chunks per d-half (128 B per row)
-      for (int i = C.tid - 64; i < 2 * nz; i += 128) {
+      for (int i = C.tid - 384; i < 2 * nz; i += 128) {
         const int hf = i / nz, j = i - hf * nz;
         *reinterpret_cast<uint4 *>(vt + hf * 8192 + nvalid * 128 + j * 16) = make_uint4(0u, 0u, 0u, 0u);
       }
