@@ -908,13 +908,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
               ml.y > 0.f ? (ml.x + __log2f(ml.y)) * 0.69314718055994531f : -INFINITY;
         }
       }
-      // publish: this item's partials of (request, KV head) are complete (release)
-      __threadfence();
+      // hand O^T / (m, l) back, then publish the item: the barrier orders every epilogue
+      // thread's partial stores before one thread's gpu-scope fence + counter increment
+      // (release pattern), so only that thread waits for the stores to drain
       named_bar_sync(2, 128);
-      if (etid == 0) atomicAdd(p.done + x.r * kGroup + x.g, 1);
       if (warp == 6 && lane == 0) trace_ev(p, 11, 2048 + item_idx);
       tc_fence_before();
       mbar_arrive(o_free + ob);
+      if (etid == 0) {
+        __threadfence();
+        atomicAdd(p.done + x.r * kGroup + x.g, 1);
+      }
     }
   }
   tc_fence_before();
