@@ -39,8 +39,14 @@ namespace taper {
 constexpr int kTile = kTileTokens;   // 64 tokens per pipeline stage
 // K and V tiles ride separate TMA rings: a K stage is released as soon as QK(t) completes,
 // a V stage only after PV(t); each stage is 64 tokens x 128 d bf16 = 16 KB.
-constexpr int kKStages = 5;
-constexpr int kVStages = 5;
+#ifndef TAPER_KSTAGES
+#define TAPER_KSTAGES 5
+#endif
+#ifndef TAPER_VSTAGES
+#define TAPER_VSTAGES 5
+#endif
+constexpr int kKStages = TAPER_KSTAGES;
+constexpr int kVStages = TAPER_VSTAGES;
 constexpr int kStageBytes = 2 * 8192;
 constexpr int kOffV = kKStages * kStageBytes;
 constexpr int kOffQ = kOffV + kVStages * kStageBytes;   // Q^T operand, 2 buffers x 64 rows
