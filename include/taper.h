@@ -80,12 +80,22 @@ typedef enum {
   TAPER_POLICY_GREEDY = 3 /* TAPER: Alg. 1 greedy under the slack budget               */
 } taper_policy_kind;
 
+/* What the latency model's L_context counts (App. C.1).                        */
+typedef enum {
+  TAPER_CTX_PER_SEQUENCE = 0, /* the paper's reading: every admitted sequence counts its
+                                 whole context Lsh_r + Lloc_s ([C-adm-6], L318)         */
+  TAPER_CTX_PER_REQUEST = 1   /* cascade-aware: request r's prefix
+                                 counts once, each admitted slot adds its Lloc_s -- the
+                                 bytes taper_decode_attention actually reads           */
+} taper_ctx_counting;
+
 typedef struct {            /* [host] */
   int32_t kind;             /* taper_policy_kind                                       */
   int32_t cap;              /* TAPER_POLICY_CAP: k >= 1                                */
   double rho;               /* slack fraction, (0, 1] (Sec. 3.3; default 0.8 L391) */
   const double *marginal_utility; /* must be NULL = linear utility u_r(k) = k (L391);
                                      non-linear curves return TAPER_ERR_UNSUPPORTED    */
+  int32_t ctx_counting;     /* taper_ctx_counting (0 = the paper's per-sequence count) */
 } taper_policy;
 
 /* Batch state, structure-of-arrays (device).  Request r's ready slots are the slot

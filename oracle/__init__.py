@@ -29,6 +29,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 POLICY_OFF, POLICY_CAP, POLICY_EAGER, POLICY_GREEDY = 0, 1, 2, 3
 POLICY_IDS = {"off": POLICY_OFF, "cap": POLICY_CAP, "eager": POLICY_EAGER,
               "taper": POLICY_GREEDY, "greedy": POLICY_GREEDY}
+CTX_IDS = {"per_sequence": 0, "per_request": 1}
 
 
 def build(force: bool = False) -> str:
@@ -57,6 +58,12 @@ def _load():
         lib.oracle_admit.restype = ctypes.c_int
         lib.oracle_admit.argtypes = [i32, i32, P, P, P, P, f64, f64, f64, i32, i32, f64,
                                      P, i32, P, P, P, P]
+        lib.oracle_admit_ctx.restype = ctypes.c_int
+        lib.oracle_admit_ctx.argtypes = [i32, i32, P, P, P, P, f64, f64, f64, i32, i32, f64,
+                                         P, i32, i32, P, P, P, P]
+        lib.oracle_bruteforce_ctx.restype = ctypes.c_int
+        lib.oracle_bruteforce_ctx.argtypes = [i32, i32, P, P, P, P, f64, f64, f64, f64, P, i32,
+                                              i32, P, P, P, P]
         lib.oracle_bruteforce.restype = ctypes.c_int
         lib.oracle_bruteforce.argtypes = [i32, i32, P, P, P, P, f64, f64, f64, f64, P, i32,
                                           P, P, P, P]
@@ -103,10 +110,12 @@ class Admission:
 
 
 def admit(req_shared_len, req_slot_off, req_slack_ms, slot_local_len, model, policy="taper",
-          cap=2, rho=0.8, utility=None) -> Admission:
+          cap=2, rho=0.8, utility=None, ctx="per_sequence") -> Admission:
     """Alg. 1 literally, or a fixed policy (App. D).
 
     ``model`` = (a, b, c); ``utility`` = None (linear) or [R, K] table u_r(k).
+    ``ctx`` = "per_sequence" (the paper's L_context, [C-adm-6]) or "per_request" (the
+    prefix counted once per request, NEXT-1).
     """
     Lsh, off, Lloc = _i32(req_shared_len), _i32(req_slot_off), _i32(slot_local_len)
     slack = _f64(req_slack_ms)
@@ -118,16 +127,16 @@ def admit(req_shared_len, req_slot_off, req_slack_ms, slot_local_len, model, pol
     util = None if utility is None else _f64(utility)
     ustride = 0 if util is None else util.shape[1]
     a, b, c = (float(x) for x in model)
-    st = _load().oracle_admit(R, S, _p(Lsh), _p(off), _p(slack), _p(Lloc), a, b, c,
-                              POLICY_IDS[policy], int(cap), float(rho), _p(util), ustride,
-                              _p(width), _p(adm), _p(diag), _p(nev))
+    st = _load().oracle_admit_ctx(R, S, _p(Lsh), _p(off), _p(slack), _p(Lloc), a, b, c,
+                                  POLICY_IDS[policy], int(cap), float(rho), _p(util), ustride,
+                                  CTX_IDS[ctx], _p(width), _p(adm), _p(diag), _p(nev))
     if st < 0:
         raise ValueError(f"oracle_admit error {st}")
     return Admission(st, width, adm, *diag.tolist(), int(nev[0]))
 
 
 def bruteforce(req_shared_len, req_slot_off, req_slack_ms, slot_local_len, model, rho=0.8,
-               utility=None):
+               utility=None, ctx="per_sequence"):
     """App. B (L290-296): best sum_r u_r(k_r) over all feasible subsets.
 
     Returns (best_utility, best_mask, n_opp, budget)."""
@@ -140,9 +149,9 @@ def bruteforce(req_shared_len, req_slot_off, req_slack_ms, slot_local_len, model
     no = np.zeros(1, np.int32)
     bg = np.zeros(1, np.float64)
     a, b, c = (float(x) for x in model)
-    st = _load().oracle_bruteforce(len(Lsh), len(Lloc), _p(Lsh), _p(off), _p(slack), _p(Lloc),
-                                   a, b, c, float(rho), _p(util), ustride, _p(bu), _p(bm),
-                                   _p(no), _p(bg))
+    st = _load().oracle_bruteforce_ctx(len(Lsh), len(Lloc), _p(Lsh), _p(off), _p(slack),
+                                       _p(Lloc), a, b, c, float(rho), _p(util), ustride,
+                                       CTX_IDS[ctx], _p(bu), _p(bm), _p(no), _p(bg))
     if st < 0:
         raise ValueError(f"oracle_bruteforce error {st}")
     return float(bu[0]), int(bm[0]), int(no[0]), float(bg[0])

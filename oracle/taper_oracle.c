@@ -96,17 +96,21 @@ static double utility(const double *util, int32_t ustride, int32_t r, int32_t k)
  *   Lsh[r] = shared-segment length (serial request: whole context);
  *   Lloc[s] = branch-local length of slot s; slack[r] = d_r(t) - t in ms.
  *   Each admitted slot of r contributes Lsh[r] + Lloc[s] context tokens
- *   (per-sequence counting, L318 "their aggregate context length" [C-adm-6]).
+ *   (per-sequence counting, L318 "their aggregate context length" [C-adm-6]);
+ *   oracle_admit_ctx with ctx_per_request = 1 counts r's prefix once: its first
+ *   (protected) slot adds Lsh[r] + Lloc[s], every further slot only Lloc[s] (the
+ *   bytes a cascade kernel reads, reading R-ctx).
  * Outputs: req_width[r] = w_{r,t} (0 for a request with no ready slot),
  *   slot_admitted[s] in {0,1}, diag = {T0, budget, T(S), E = T(S)-T0, min_slack},
  *   *n_evals = number of T() evaluations performed by the greedy loop.
  * Returns ORACLE_OK, ORACLE_STATUS_EMPTY_REQUEST, or a negative error.
  */
-int oracle_admit(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *off,
-                 const double *slack, const int32_t *Lloc, double a, double b,
-                 double c, int32_t kind, int32_t cap, double rho,
-                 const double *util, int32_t ustride, int32_t *req_width,
-                 uint8_t *slot_admitted, double *diag, int64_t *n_evals) {
+int oracle_admit_ctx(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *off,
+                     const double *slack, const int32_t *Lloc, double a, double b,
+                     double c, int32_t kind, int32_t cap, double rho,
+                     const double *util, int32_t ustride, int32_t ctx_per_request,
+                     int32_t *req_width, uint8_t *slot_admitted, double *diag,
+                     int64_t *n_evals) {
   if (R < 0 || S < 0 || off[0] != 0 || off[R] != S) return ORACLE_ERR_ARG;
   int status = ORACLE_OK;
   int32_t *order = (int32_t *)malloc(sizeof(int32_t) * (size_t)(S > 0 ? S : 1));
@@ -147,7 +151,7 @@ int oracle_admit(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *off,
         int32_t s = order[off[r] + p];
         slot_admitted[s] = 1;
         n += 1;
-        L += (int64_t)Lsh[r] + (int64_t)Lloc[s];
+        L += (ctx_per_request ? 0 : (int64_t)Lsh[r]) + (int64_t)Lloc[s];
       }
       req_width[r] = w;
     }
@@ -169,7 +173,7 @@ int oracle_admit(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *off,
         if (!cand[r]) continue;
         /* AddBranch(step, r): r's next ready branch in canonical order. */
         int32_t s = order[off[r] + 1 + granted[r]];
-        int64_t dL = (int64_t)Lsh[r] + (int64_t)Lloc[s];
+        int64_t dL = (ctx_per_request ? 0 : (int64_t)Lsh[r]) + (int64_t)Lloc[s];
         double T_widened = oracle_T(a, b, c, n + 1, L + dL);
         evals += 1;
         /* Alg. 1 lines 12-14: monotone: prune request r. */
@@ -223,6 +227,15 @@ int oracle_admit(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *off,
   return status;
 }
 
+int oracle_admit(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *off,
+                 const double *slack, const int32_t *Lloc, double a, double b,
+                 double c, int32_t kind, int32_t cap, double rho,
+                 const double *util, int32_t ustride, int32_t *req_width,
+                 uint8_t *slot_admitted, double *diag, int64_t *n_evals) {
+  return oracle_admit_ctx(R, S, Lsh, off, slack, Lloc, a, b, c, kind, cap, rho, util, ustride,
+                          0, req_width, slot_admitted, diag, n_evals);
+}
+
 /*
  * oracle_bruteforce: App. B width-allocation problem on a tiny batch.
  * Enumerates every subset of the opportunistic slots (all ready slots except
@@ -231,11 +244,11 @@ int oracle_admit(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *off,
  * best_mask receives the lexicographically-first optimal subset as a bitmask
  * over opportunistic slots listed in ascending slot index; *n_opp their count.
  */
-int oracle_bruteforce(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *off,
-                      const double *slack, const int32_t *Lloc, double a, double b,
-                      double c, double rho, const double *util, int32_t ustride,
-                      double *best_utility, int64_t *best_mask, int32_t *n_opp_out,
-                      double *budget_out) {
+int oracle_bruteforce_ctx(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *off,
+                          const double *slack, const int32_t *Lloc, double a, double b,
+                          double c, double rho, const double *util, int32_t ustride,
+                          int32_t ctx_per_request, double *best_utility, int64_t *best_mask,
+                          int32_t *n_opp_out, double *budget_out) {
   if (R < 0 || S < 0 || off[0] != 0 || off[R] != S) return ORACLE_ERR_ARG;
   int32_t *order = (int32_t *)malloc(sizeof(int32_t) * (size_t)(S > 0 ? S : 1));
   int32_t opp_slot[24], opp_req[24];
@@ -271,7 +284,7 @@ int oracle_bruteforce(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *o
     for (int32_t i = 0; i < n_opp; ++i)
       if (mask & ((int64_t)1 << i)) {
         n += 1;
-        L += (int64_t)Lsh[opp_req[i]] + (int64_t)Lloc[opp_slot[i]];
+        L += (ctx_per_request ? 0 : (int64_t)Lsh[opp_req[i]]) + (int64_t)Lloc[opp_slot[i]];
         k[opp_req[i]] += 1;
       }
     if (oracle_T(a, b, c, n, L) > budget) continue;
@@ -287,6 +300,15 @@ int oracle_bruteforce(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *o
   free(is_prot);
   free(k);
   return ORACLE_OK;
+}
+
+int oracle_bruteforce(int32_t R, int32_t S, const int32_t *Lsh, const int32_t *off,
+                      const double *slack, const int32_t *Lloc, double a, double b,
+                      double c, double rho, const double *util, int32_t ustride,
+                      double *best_utility, int64_t *best_mask, int32_t *n_opp_out,
+                      double *budget_out) {
+  return oracle_bruteforce_ctx(R, S, Lsh, off, slack, Lloc, a, b, c, rho, util, ustride, 0,
+                               best_utility, best_mask, n_opp_out, budget_out);
 }
 
 /* bf16 bit pattern -> exact fp64 value. */

@@ -26,6 +26,7 @@ struct AdmitParams {
   const double *slack;
   double a, b, c, rho;
   int kind, cap;
+  int ctx_per_request;  // TAPER_CTX_PER_REQUEST: an opportunistic slot adds Lloc only
   int decide;  // 1: admission + work list; 0: work list from slot_admitted only
   int32_t *req_width;
   uint8_t *slot_admitted;
@@ -197,7 +198,9 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
           bool active = r >= 0 && r < R;
           uint8_t adm = prot ? 1 : 0;
           if (active && !prot) {
-            long long dL = (long long)p.Lsh[r] + (long long)p.Lloc[s];
+            // context added by admitting s: its whole sequence (paper, per sequence) or
+            // only its local segment (cascade-aware, the prefix already counted once)
+            long long dL = (p.ctx_per_request ? 0ll : (long long)p.Lsh[r]) + (long long)p.Lloc[s];
             if (p.kind == TAPER_POLICY_EAGER) {
               adm = 1; my_nadd += 1; my_Ladd += dL;
             } else if (p.kind == TAPER_POLICY_CAP) {
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
             if (i - first < p.cap - 1) {
               p.slot_admitted[s] = 1;
               my_nadd += 1;
-              my_Ladd += (long long)p.Lsh[r] + (long long)p.Lloc[s];
+              my_Ladd += (p.ctx_per_request ? 0ll : (long long)p.Lsh[r]) + (long long)p.Lloc[s];
             }
           }
         } else {
@@ -511,6 +514,9 @@ static int launch_admit(const taper_batch *batch, const taper_latency_model *mod
       return fail(TAPER_ERR_UNSUPPORTED, "only linear utility is implemented on the device");
     p.a = model->a; p.b = model->b; p.c = model->c; p.rho = policy->rho;
     p.kind = policy->kind; p.cap = policy->cap;
+    if (policy->ctx_counting != TAPER_CTX_PER_SEQUENCE && policy->ctx_counting != TAPER_CTX_PER_REQUEST)
+      return fail(TAPER_ERR_ARG, "ctx_counting must be TAPER_CTX_PER_SEQUENCE or _PER_REQUEST");
+    p.ctx_per_request = policy->ctx_counting == TAPER_CTX_PER_REQUEST;
   }
   WsLayout L = ws_layout(R, S);
   if (ws_bytes < L.fixed) return fail(TAPER_ERR_CAPACITY, "workspace smaller than the fixed part");

@@ -36,7 +36,10 @@ class _Model(ctypes.Structure):
 
 class _Policy(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("cap", ctypes.c_int32), ("rho", ctypes.c_double),
-                ("marginal_utility", _vp)]
+                ("marginal_utility", _vp), ("ctx_counting", ctypes.c_int32)]
+
+
+CTX_COUNTING = {"per_sequence": 0, "per_request": 1}
 
 
 class _Batch(ctypes.Structure):
@@ -233,12 +236,13 @@ def taper_workspace_size(n_req: int, n_slot: int, h_local: int, max_chunk_slots:
 
 def taper_admit(batch: DeviceBatch, model, policy: str = "taper", rho: float = 0.8,
                 adm: DeviceAdmission = None, h_local: int = 8, workspace: torch.Tensor = None,
-                cap: int = 2, stream=None) -> DeviceAdmission:
+                cap: int = 2, stream=None, ctx: str = "per_sequence") -> DeviceAdmission:
     a, b, c = (float(x) for x in model)
     kind = POLICY[policy] if isinstance(policy, str) else int(policy)
     bc, ac = batch.c(), adm.c()
     _check(_lib.taper_admit(ctypes.byref(bc), ctypes.byref(_Model(a, b, c)),
-                            ctypes.byref(_Policy(kind, cap, rho, None)), ctypes.byref(ac),
+                            ctypes.byref(_Policy(kind, cap, rho, None, CTX_COUNTING[ctx])),
+                            ctypes.byref(ac),
                             h_local, _ptr(workspace), workspace.numel() * workspace.element_size(),
                             _stream(stream)), "taper_admit")
     return adm

@@ -10,22 +10,22 @@ import synth
 pytestmark = pytest.mark.gpu
 
 
-def _gpu_admit(b, model, policy, rho, cap=2, h=8):
+def _gpu_admit(b, model, policy, rho, cap=2, h=8, ctx="per_sequence"):
     from paper_2605_06914_b200 import taper as T
     db = T.DeviceBatch.from_host(b)
     adm = T.DeviceAdmission.empty(b.n_req, b.n_slot)
     ws = torch.empty(T.taper_workspace_size(b.n_req, b.n_slot, h,
                                             T.max_chunk_slots(b.req_shared_len, b.req_slot_off, b.slot_local_len)),
                      dtype=torch.uint8, device="cuda")
-    T.taper_admit(db, model, policy, rho, adm, h, ws, cap)
+    T.taper_admit(db, model, policy, rho, adm, h, ws, cap, ctx=ctx)
     torch.cuda.synchronize()
     return adm
 
 
-def _compare(b, model, policy, rho, cap=2):
-    g = _gpu_admit(b, model, policy, rho, cap)
+def _compare(b, model, policy, rho, cap=2, ctx="per_sequence"):
+    g = _gpu_admit(b, model, policy, rho, cap, ctx=ctx)
     o = oracle.admit(b.req_shared_len, b.req_slot_off, b.req_slack_ms, b.slot_local_len, model,
-                     policy, cap, rho)
+                     policy, cap, rho, ctx=ctx)
     R, S = b.n_req, b.n_slot
     np.testing.assert_array_equal(g.req_width.cpu().numpy()[:R], o.req_width)
     np.testing.assert_array_equal(g.slot_admitted.cpu().numpy()[:S], o.slot_admitted)
@@ -40,13 +40,15 @@ def _compare(b, model, policy, rho, cap=2):
     return o
 
 
+@pytest.mark.parametrize("ctx", ["per_sequence", "per_request"])
 @pytest.mark.parametrize("policy", ["off", "cap", "eager", "taper"])
-def test_random_small_batches(policy):
+def test_random_small_batches(policy, ctx):
     rng = np.random.default_rng(42)
     for i in range(300):
         b = synth.random_small_batch(rng, max_req=12, max_fanout=6, max_local=50)
         model = (rng.uniform(0, 20), rng.uniform(1e-3, 0.1), rng.uniform(1e-5, 1e-2))
-        _compare(b, model, policy, float(rng.uniform(0.05, 1.0)), cap=int(rng.integers(1, 6)))
+        _compare(b, model, policy, float(rng.uniform(0.05, 1.0)), cap=int(rng.integers(1, 6)),
+                 ctx=ctx)
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])

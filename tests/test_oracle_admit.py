@@ -258,3 +258,55 @@ def test_zero_requests():
     b = _batch([], [], [], [])
     a = _admit(b, (3, .1, .01))
     assert a.T0 == 3.0 and a.budget == 3.0 and a.min_slack == np.inf
+
+
+# ---- cascade-aware context counting (reading R-ctx)
+
+def test_per_request_worked_example():
+    """One request, prefix 1000, branches Lloc 10/20/30/40, T = 1 + 0.1 n + 0.001 L (ms),
+    rho = 1, min slack 3.5 ms (budget 3.5).  Worked by hand:
+      T0 = 1 + 0.1 + 0.001 * 1010 = 2.11.
+      per sequence: +20 -> L 2030, T 3.23 <= 3.5; +30 -> L 3060, T 4.36 > 3.5: width 2.
+      per request:  +20 -> L 1030, T 2.23; +30 -> 1060, 2.36; +40 -> 1100, 2.50: width 4."""
+    args = ([1000], [0, 4], [3.5], [10, 20, 30, 40], (1.0, 0.1, 0.001))
+    seq = oracle.admit(*args, policy="taper", rho=1.0, ctx="per_sequence")
+    req = oracle.admit(*args, policy="taper", rho=1.0, ctx="per_request")
+    assert seq.req_width.tolist() == [2] and seq.slot_admitted.tolist() == [1, 1, 0, 0]
+    assert req.req_width.tolist() == [4] and req.slot_admitted.tolist() == [1, 1, 1, 1]
+    assert abs(seq.T_S - 3.23) < 1e-12 and abs(req.T_S - 2.50) < 1e-12
+    assert abs(req.T0 - 2.11) < 1e-12 and req.T0 == seq.T0  # S0 counts each prefix once anyway
+
+
+def test_per_request_eager_closed_form():
+    """Eager admits every slot; per-request counting makes T(S) = a + b S + c (sum Lsh +
+    sum Lloc) -- each prefix once -- checked against integers summed here."""
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        b = synth.random_small_batch(rng, max_req=6, max_fanout=5, max_local=80)
+        o = oracle.admit(b.req_shared_len, b.req_slot_off, b.req_slack_ms, b.slot_local_len,
+                         (2.0, 0.25, 0.5), "eager", ctx="per_request")
+        n = int(b.n_slot)
+        L = int(np.sum(b.req_shared_len)) + int(np.sum(b.slot_local_len))
+        assert o.T_S == (2.0 + 0.25 * n) + 0.5 * L
+
+
+def test_per_request_greedy_is_optimal_and_dominates():
+    """Linear utility, costs additive in (n, L): cheapest-first is optimal under any
+    monotone threshold (theorem), so greedy == brute force also for the
+    cascade-aware count; and per-request admits a superset of per-sequence (every
+    candidate is cheaper, the budget is the same)."""
+    rng = np.random.default_rng(11)
+    for _ in range(200):
+        b = synth.random_small_batch(rng, max_req=5, max_fanout=4, max_shared=2000, max_local=40)
+        model = (rng.uniform(0, 20), rng.uniform(1e-3, 0.1), rng.uniform(1e-5, 1e-2))
+        rho = float(rng.uniform(0.1, 1.0))
+        req = oracle.admit(b.req_shared_len, b.req_slot_off, b.req_slack_ms, b.slot_local_len,
+                           model, "taper", rho=rho, ctx="per_request")
+        seq = oracle.admit(b.req_shared_len, b.req_slot_off, b.req_slack_ms, b.slot_local_len,
+                           model, "taper", rho=rho, ctx="per_sequence")
+        best, _, n_opp, budget = oracle.bruteforce(b.req_shared_len, b.req_slot_off,
+                                                   b.req_slack_ms, b.slot_local_len, model,
+                                                   rho=rho, ctx="per_request")
+        assert req.req_width.sum() - b.n_req == best
+        assert req.T_S <= budget
+        assert np.all(req.slot_admitted >= seq.slot_admitted)
