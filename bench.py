@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--config", default="c2", choices=list(WORKLOADS))
     ap.add_argument("--layers", type=int, default=synth.N_LAYERS)
     ap.add_argument("--policy", default="taper", choices=["taper", "eager", "off", "cap"])
+    ap.add_argument("--ctx", default="per_sequence", choices=["per_sequence", "per_request"],
+                    help="L_context of the latency model: the paper's per-sequence count or "
+                         "the cascade-aware per-request count (NEXT-1)")
     ap.add_argument("--slack-x", type=float, default=2.0,
                     help="min slack = T0 + x (T_eager - T0)/rho; x >= 1 admits every branch")
     ap.add_argument("--seed", type=int, default=0)
@@ -288,7 +291,7 @@ def run_ours(args):
         n = 0
         if adm_ev is not None:
             adm_ev[0].record(stream)
-        T.taper_admit(db, MODEL, args.policy, RHO, adm, h, ws, 2)
+        T.taper_admit(db, MODEL, args.policy, RHO, adm, h, ws, 2, ctx=args.ctx)
         n += T.taper_last_launch_count()
         if G > 1:
             par.broadcast_admission(adm.slot_admitted)
@@ -391,7 +394,8 @@ def run_ours(args):
             "dtype": "bf16", "data": "synthetic (seeded N(0,1) bf16 K/V/q; no model weights)",
             "config": {
                 "workload": f"{args.config}: {WORKLOADS[args.config]}",
-                "policy": args.policy, "rho": RHO, "latency_model_ms": list(MODEL),
+                "policy": args.policy, "ctx_counting": args.ctx, "rho": RHO,
+                "latency_model_ms": list(MODEL),
                 "slack_x": args.slack_x, "admitted_slots": int(adm_mask.sum()),
                 "ready_slots": S, "requests": R, "layers": L,
                 "kv_layer_buffers": n_distinct,
@@ -470,7 +474,7 @@ def run_e2e(args, T, torch, dist, G, batch, db, adm, ws, kvs, L, S, h, scale, de
                 dq[l].copy_(host_q[l], non_blocking=True)
                 q_ready[l].record(h2d)
         comp.wait_event(state_ready)
-        T.taper_admit(db, MODEL, args.policy, RHO, adm, h, ws, 2)
+        T.taper_admit(db, MODEL, args.policy, RHO, adm, h, ws, 2, ctx=args.ctx)
         if G > 1:
             par.broadcast_admission(adm.slot_admitted)
             T.taper_build_work(db, adm, h, ws)
