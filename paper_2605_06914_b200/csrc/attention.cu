@@ -5,23 +5,26 @@
 // and "a backend with paged or radix-tree KV caches can serve all branches from a single
 // set of prefix blocks".  Two kernels:
 //
-//  A6+A7  attend_kernel (tcgen05 + TMA, one persistent CTA per SM)
-//     Work items of one request r and local KV head g, all sharing the same stacked query
-//     operand Q_stack = [8 GQA heads] x [w_r admitted branches] (rows = 8 w_r <= 128):
-//       * shared item : one 1024-token chunk of P (+) H -- every page read ONCE from HBM
-//                       and contracted against all stacked rows (the cascade);
-//       * local item  : up to 16 64-token tiles of the branches' own segments h_i (+) y_i,
-//                       each tile masked to the 8 rows of the branch that owns it.
-//     Per 64-token tile:  S = Q_stack K^T (tcgen05.mma, A = Q in TMEM, B = K via TMA in
-//     SMEM, fp32 S in TMEM) -> online softmax (one TMEM lane per row) -> P = hi + lo bf16
-//     written back into the S columns of TMEM -> O += P V (tcgen05.mma, A = P in TMEM,
-//     B = V straight from the TMA tile as an MN-major operand).  When <= 32 (<= 64) rows
-//     are live, Q_stack is replicated into 4 (2) TMEM lane quadrants and each copy owns a
-//     16 (32)-token slice of every tile (split-K inside the CTA, PV lanes masked per copy),
-//     so the softmax work is spread over all four SM sub-partitions; the copies are merged
-//     in the epilogue.  Output: a normalised partial (o, lse) per stacked row and item.
+//  A6+A7  attend_kernel (tcgen05 + TMA, one persistent CTA per SM, dynamic scheduling)
+//     Work items of one request r and local KV head g; the stacked query operand is
+//     Q^T = [8 GQA heads] x [w admitted branches] (N = 8 w <= 64 rows):
+//       * shared item : one 1024-token chunk of P (+) H for a group of <= 8 admitted
+//                       branches -- every page read ONCE from HBM and contracted against
+//                       all stacked rows (the cascade);
+//       * local item  : <= 16 64-token tiles of ONE admitted branch's h_i (+) y_i (w = 1).
+//     Per 64-token tile, "swap-AB" (tokens on the MMA's M, stacked rows on N):
+//       S^T = K Q^T    tcgen05.mma SS, M = 64 tokens, N = 8 w, K = 128 (A = the K tile by
+//                      TMA, B = Q^T by TMA, both SMEM; fp32 S^T in TMEM)
+//       online softmax (two groups of 4 warps; lazy running max) -> P = hi + lo bf16,
+//                      stored transposed into SMEM with stmatrix.trans
+//       O^T += V^T P^T tcgen05.mma SS, M = 128 (d), N = 16 w (hi and lo rows), K = 64
+//                      (A = the V tile as an MN-major operand, B = P^T)
+//     so the tensor and softmax work of a tile scale with the live rows.  Output: a
+//     normalised partial (o, lse) per stacked row and item, published per (request, KV
+//     head) on a completion counter.
 //  A8     merge_kernel: per admitted slot and KV head, log-sum-exp merge of its partials
-//     (prefix chunks in order, then local items) into bf16 out[s, 8g:8g+8, :].
+//     (prefix chunks in order, then its local items) into bf16 out[s, 8g:8g+8, :];
+//     launched with PDL, each warp starts once its request's items are published.
 //
 // Item boundaries depend only on segment lengths, and a stacked row's arithmetic does not
 // depend on which other rows share the operand, so a slot's output does not depend on
