@@ -137,8 +137,11 @@ typedef struct {
 } taper_kv;
 
 /* Workspace bytes for a batch of at most n_req requests / n_slot slots on a rank with
- * h_local KV heads, where max_chunk_slots bounds sum_r w_r * ceil(Lsh_r / 1024) (the
- * Eager value sum_r n_r * ceil(Lsh_r/1024) is always enough).  [host]                   */
+ * h_local KV heads.  max_chunk_slots bounds the partial rows' count
+ *     sum_r w_r * ceil(Lsh_r / 1024)  +  sum_{s admitted} ceil(Lloc_s / 1024)
+ * (prefix chunks per admitted branch, plus one per local item of <= 16 64-token tiles);
+ * the Eager value of that sum over all ready slots is always enough.  An undersized
+ * workspace is reported as TAPER_STATUS_WORK_OVERFLOW, never overrun.  [host]           */
 TAPER_API int taper_workspace_size(int32_t n_req, int32_t n_slot, int32_t h_local,
                          int64_t max_chunk_slots, size_t *bytes);
 

@@ -211,19 +211,17 @@ TAPER_LOCAL_ITEM_TILES = 16
 
 
 def max_chunk_slots(req_shared_len, req_slot_off, slot_local_len) -> int:
-    """Eager-case bound on sum_r w_r * (prefix chunks + local items) of request r, for
-    taper_workspace_size (prefix chunks of 1024 tokens; local items of up to 16 64-token
-    tiles of the branches' own segments)."""
+    """Eager-case partial-row count for taper_workspace_size: per request, its ready
+    branches x prefix chunks of 1024 tokens, plus one local item per <= 16 64-token tiles
+    of each branch's own segment (include/taper.h)."""
     lsh = np.asarray(req_shared_len, np.int64)
     off = np.asarray(req_slot_off, np.int64)
     lloc = np.asarray(slot_local_len, np.int64)
     n = off[1:] - off[:-1]
     chunks = (lsh + TAPER_CHUNK_TOKENS - 1) // TAPER_CHUNK_TOKENS
-    tiles = (lloc + TAPER_TILE_TOKENS - 1) // TAPER_TILE_TOKENS
-    lt = np.add.reduceat(tiles, off[:-1]) if len(tiles) else np.zeros(len(n), np.int64)
-    lt = np.where(n > 0, lt, 0)
-    local_items = (lt + TAPER_LOCAL_ITEM_TILES - 1) // TAPER_LOCAL_ITEM_TILES
-    return int((n * (chunks + local_items)).sum())
+    per_item = TAPER_TILE_TOKENS * TAPER_LOCAL_ITEM_TILES
+    local_items = (lloc + per_item - 1) // per_item
+    return int((n * chunks).sum() + local_items.sum())
 
 
 # ------------------------------------------------------------------ C-ABI calls
