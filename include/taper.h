@@ -62,8 +62,10 @@ extern "C" {
 #define TAPER_MAX_SLOTS 4096   /* capacity of the single-CTA admission kernel (R and S)  */
 #define TAPER_HEAD_DIM 128     /* Qwen3-32B head_dim                     */
 #define TAPER_GQA_GROUP 8      /* 64 Q heads / 8 KV heads (L359)                         */
-#define TAPER_CHUNK_TOKENS 1024 /* shared-prefix split size: a fixed function of the
+#ifndef TAPER_CHUNK_TOKENS
+#define TAPER_CHUNK_TOKENS 2048 /* shared-prefix split size: a fixed function of the
                                    prefix length only (schedule invariance, Lemma 1)     */
+#endif
 
 /* App. C.1 display eq. (L316): T(S) = a + b*n_tokens + c*L_context, in ms. [host]      */
 typedef struct {
@@ -138,7 +140,7 @@ typedef struct {
 
 /* Workspace bytes for a batch of at most n_req requests / n_slot slots on a rank with
  * h_local KV heads.  max_chunk_slots bounds the partial rows' count
- *     sum_r w_r * ceil(Lsh_r / 1024)  +  sum_{s admitted} ceil(Lloc_s / 1024)
+ *     sum_r w_r * ceil(Lsh_r / TAPER_CHUNK_TOKENS)  +  sum_{s admitted} ceil(Lloc_s / 1024)
  * (prefix chunks per admitted branch, plus one per local item of <= 16 64-token tiles);
  * the Eager value of that sum over all ready slots is always enough.  An undersized
  * workspace is reported as TAPER_STATUS_WORK_OVERFLOW, never overrun.  [host]           */

@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
   }
 
   // ---- work list (A5): per-request widths, item counts and CSR offsets.
-  // Shared items: (1024-token prefix chunk, group of <= 8 admitted branches).  Local items:
+  // Shared items: (TAPER_CHUNK_TOKENS prefix chunk, group of <= 8 admitted branches).  Local items:
   // <= kLocalItemTiles 64-token tiles of ONE admitted branch's local KV.  Partials (8 rows
   // per KV head each): shared (chunk c, branch j) at c * w + j, then one per local item.
   int w_loc[kPerThread], nc_loc[kPerThread], nl_loc[kPerThread], cs_loc[kPerThread];

@@ -8,7 +8,7 @@
 //  A6+A7  attend_kernel (tcgen05 + TMA, one persistent CTA per SM, dynamic scheduling)
 //     Work items of one request r and local KV head g; the stacked query operand is
 //     Q^T = [8 GQA heads] x [w admitted branches] (N = 8 w <= 64 rows):
-//       * shared item : one 1024-token chunk of P (+) H for a group of <= 8 admitted
+//       * shared item : one 2048-token chunk of P (+) H for a group of <= 8 admitted
 //                       branches -- every page read ONCE from HBM and contracted against
 //                       all stacked rows (the cascade);
 //       * local item  : <= 16 64-token tiles of ONE admitted branch's h_i (+) y_i (w = 1).
@@ -40,6 +40,9 @@
 namespace taper {
 
 constexpr int kTile = kTileTokens;   // 64 tokens per pipeline stage
+constexpr int kItemTiles = (kChunk / kTileTokens > kLocalItemTiles) ? kChunk / kTileTokens
+                                                                    : kLocalItemTiles;
+static_assert(kItemTiles <= 32, "one scheduler lane resolves one tile of an item");
 // K and V tiles ride separate TMA rings: a K stage is released as soon as QK(t) completes,
 // a V stage only after PV(t); each stage is 64 tokens x 128 d bf16 = 16 KB.
 #ifndef TAPER_KSTAGES
@@ -64,9 +67,9 @@ constexpr int kOffML = kOffPT + kPTBytes;  // (m, l) of the 64 stacked rows, 2 b
 constexpr int kRedFloats = 3 * 4 * 64;
 constexpr int kOffRed = kOffML + 2 * 64 * 8;
 constexpr int kOffAlpha = kOffRed + 2 * kRedFloats * 4;  // per-warp rescale factors [8][64]
-constexpr int kItemRing = 8;                  // claimed-item ring (ItemRec, 512 B each)
+constexpr int kItemRing = 8;                  // claimed-item ring (ItemRec records)
 constexpr int kOffRec = kOffAlpha + 8 * 64 * 4;
-constexpr int kOffBar = kOffRec + kItemRing * 512;
+constexpr int kOffBar = kOffRec + kItemRing * 1024;
 constexpr int kSmemUsed = kOffBar + 512;
 constexpr int kSmemBytes = kSmemUsed + 1024;  // + alignment slack
 // warp 0: K producer; warp 1: MMA issuer; warps 2-5: softmax group 0; warps 6-9:
@@ -110,10 +113,10 @@ struct Item {
 struct ItemRec {
   int32_t it, g, desc[8];  // desc = ItemDesc {r, w, adm_off, cs0, tb, te, nt, flags}
   int32_t pad[6];
-  int32_t tok0[kLocalItemTiles], valid[kLocalItemTiles], spare[kLocalItemTiles];
-  int32_t pg[kLocalItemTiles][4];
+  int32_t tok0[kItemTiles], valid[kItemTiles];
+  int32_t pg[kItemTiles][4];
 };
-static_assert(sizeof(ItemRec) == 512, "ItemRec size");
+static_assert(sizeof(ItemRec) <= 1024, "ItemRec size");
 
 __device__ __forceinline__ void decode_item(const ItemRec *rec, Item &x) {
   x.g = rec->g;
