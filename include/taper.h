@@ -63,7 +63,7 @@ extern "C" {
 #define TAPER_HEAD_DIM 128     /* Qwen3-32B head_dim                     */
 #define TAPER_GQA_GROUP 8      /* 64 Q heads / 8 KV heads (L359)                         */
 #ifndef TAPER_CHUNK_TOKENS
-#define TAPER_CHUNK_TOKENS 2048 /* shared-prefix split size: a fixed function of the
+#define TAPER_CHUNK_TOKENS 4096 /* shared-prefix split size: a fixed function of the
                                    prefix length only (schedule invariance, Lemma 1)     */
 #endif
 

@@ -8,7 +8,7 @@
 //  A6+A7  attend_kernel (tcgen05 + TMA, one persistent CTA per SM, dynamic scheduling)
 //     Work items of one request r and local KV head g; the stacked query operand is
 //     Q^T = [8 GQA heads] x [w admitted branches] (N = 8 w <= 64 rows):
-//       * shared item : one 2048-token chunk of P (+) H for a group of <= 8 admitted
+//       * shared item : one 4096-token chunk of P (+) H for a group of <= 8 admitted
 //                       branches -- every page read ONCE from HBM and contracted against
 //                       all stacked rows (the cascade);
 //       * local item  : <= 16 64-token tiles of ONE admitted branch's h_i (+) y_i (w = 1).
@@ -42,7 +42,7 @@ namespace taper {
 constexpr int kTile = kTileTokens;   // 64 tokens per pipeline stage
 constexpr int kItemTiles = (kChunk / kTileTokens > kLocalItemTiles) ? kChunk / kTileTokens
                                                                     : kLocalItemTiles;
-static_assert(kItemTiles <= 32, "one scheduler lane resolves one tile of an item");
+static_assert(kItemTiles <= 64, "scheduler lanes resolve at most two tiles each");
 // K and V tiles ride separate TMA rings: a K stage is released as soon as QK(t) completes,
 // a V stage only after PV(t); each stage is 64 tokens x 128 d bf16 = 16 KB.
 #ifndef TAPER_KSTAGES
@@ -67,9 +67,10 @@ constexpr int kOffML = kOffPT + kPTBytes;  // (m, l) of the 64 stacked rows, 2 b
 constexpr int kRedFloats = 3 * 4 * 64;
 constexpr int kOffRed = kOffML + 2 * 64 * 8;
 constexpr int kOffAlpha = kOffRed + 2 * kRedFloats * 4;  // per-warp rescale factors [8][64]
-constexpr int kItemRing = 8;                  // claimed-item ring (ItemRec records)
+constexpr int kRecBytes = kItemTiles <= 32 ? 1024 : 2048;  // ItemRec slot
+constexpr int kItemRing = 8192 / kRecBytes;   // claimed-item ring (8 KB of ItemRec records)
 constexpr int kOffRec = kOffAlpha + 8 * 64 * 4;
-constexpr int kOffBar = kOffRec + kItemRing * 1024;
+constexpr int kOffBar = kOffRec + kItemRing * kRecBytes;
 constexpr int kSmemUsed = kOffBar + 512;
 constexpr int kSmemBytes = kSmemUsed + 1024;  // + alignment slack
 // warp 0: K producer; warp 1: MMA issuer; warps 2-5: softmax group 0; warps 6-9:
@@ -116,7 +117,7 @@ struct ItemRec {
   int32_t tok0[kItemTiles], valid[kItemTiles];
   int32_t pg[kItemTiles][4];
 };
-static_assert(sizeof(ItemRec) <= 1024, "ItemRec size");
+static_assert(sizeof(ItemRec) <= kRecBytes, "ItemRec size");
 
 __device__ __forceinline__ void decode_item(const ItemRec *rec, Item &x) {
   x.g = rec->g;
@@ -662,13 +663,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         x.te = __shfl_sync(0xffffffffu, d, 5);
         x.local = __shfl_sync(0xffffffffu, d, 7) & 1;
         if (lane < 8) rec->desc[lane] = d;
-        if (lane < nt) {
-          const TileInfo ti = tile_info(p, x, lane);
-          rec->tok0[lane] = ti.tok0;
-          rec->valid[lane] = ti.valid;
+        for (int t = lane; t < nt; t += 32) {
+          const TileInfo ti = tile_info(p, x, t);
+          rec->tok0[t] = ti.tok0;
+          rec->valid[t] = ti.valid;
 #pragma unroll
           for (int b = 0; b < kTile / 16; ++b)
-            rec->pg[lane][b] =
+            rec->pg[t][b] =
                 b * box_tok < ti.valid ? __ldg(ti.pages + (ti.tok0 + b * box_tok) / p.page_size) : 0;
         }
       }

@@ -22,7 +22,7 @@ POLICY = {"off": 0, "cap": 1, "eager": 2, "taper": 3, "greedy": 3}
 TAPER_STATUS_EMPTY_REQUEST, TAPER_STATUS_BAD_LENGTH = 1, 2
 TAPER_STATUS_PRECISION, TAPER_STATUS_WORK_OVERFLOW = 4, 8
 TAPER_MAX_SLOTS = 4096
-TAPER_CHUNK_TOKENS = 2048
+TAPER_CHUNK_TOKENS = 4096
 EXPORTS = ("taper_workspace_size", "taper_admit", "taper_build_work", "taper_decode_attention",
            "taper_status_string", "taper_last_error", "taper_last_launch_count",
            "taper_set_profile_events", "taper_set_trace_buffer")

@@ -40,6 +40,6 @@ def test_host_validation_without_gpu():
         T.taper_workspace_size(10, 10, 9, 1)
     assert "monotone" in T.taper_status_string(-3)
     assert "precision" in T.taper_status_string(4)
-    # 2048-token prefix chunks x ready branches (3 x 2 + 1 x 1 + 2 x 0) + one local item per
+    # 4096-token prefix chunks x ready branches (3 x 1 + 1 x 1 + 2 x 0) + one local item per
     # branch with local tokens (65, 1, 2, 3 -> 4 items of <= 16 x 64 tokens)
-    assert T.max_chunk_slots([4096, 1, 0], [0, 3, 4, 6], [0, 65, 1, 0, 2, 3]) == 6 + 1 + 0 + 4
+    assert T.max_chunk_slots([4097, 1, 0], [0, 3, 4, 6], [0, 65, 1, 0, 2, 3]) == 6 + 1 + 0 + 4

@@ -41,10 +41,10 @@ def test_c1_tiny_all_widths(w1):
 @pytest.mark.parametrize("variant", ["flat", "peaked", "sink"])
 @pytest.mark.parametrize("page", [16, 64, 128])
 def test_multi_chunk_ragged(variant, page):
-    # prefixes spanning several 2048-token chunks with ragged tails, up to 16 branches
+    # prefixes spanning several 4096-token chunks with ragged tails, up to 16 branches
     # (128 stacked rows), serial requests, local lengths crossing page boundaries
     rng = np.random.default_rng(11)
-    lsh = [2500, 1, 64, 2047, 2049, 5000, 0, 700]
+    lsh = [2500, 1, 64, 4095, 4097, 9000, 0, 700]
     fan = [16, 1, 3, 1, 5, 2, 4, 9]
     loc = []
     for r, f in enumerate(fan):
