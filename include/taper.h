@@ -49,7 +49,7 @@ extern "C" {
 #define TAPER_ERR_CAPACITY (-4)     /* R or S > TAPER_MAX_SLOTS, page size unsupported,
                                        workspace too small                                 */
 #define TAPER_ERR_CUDA (-5)         /* a CUDA launch / driver call failed                 */
-#define TAPER_ERR_UNSUPPORTED (-6)  /* non-linear utility on the device path (round 1)    */
+#define TAPER_ERR_UNSUPPORTED (-6)  /* reserved (no call returns it at present)           */
 
 /* ----------------------------------------------------------------- device status bits */
 #define TAPER_STATUS_EMPTY_REQUEST 1   /* a request had no ready slot; it is skipped     */
@@ -95,9 +95,17 @@ typedef struct {            /* [host] */
   int32_t kind;             /* taper_policy_kind                                       */
   int32_t cap;              /* TAPER_POLICY_CAP: k >= 1                                */
   double rho;               /* slack fraction, (0, 1] (Sec. 3.3; default 0.8 L391) */
-  const double *marginal_utility; /* must be NULL = linear utility u_r(k) = k (L391);
-                                     non-linear curves return TAPER_ERR_UNSUPPORTED    */
+  const double *utility;    /* DEVICE [R][utility_stride], or NULL.  Sec. 3.4 (L142) "a
+                               monotone utility curve u_r(k)", k = opportunistic branches
+                               granted to r; Alg. 1 line 15 (L167) scores
+                               du = u_r(g+1) - u_r(g).  utility[r*stride + k] = u_r(k) for
+                               k < stride; past the table u_r is flat (u_r(stride-1)).
+                               NULL = the paper's linear utility u_r(k) = k (L391), run as
+                               sort + scan; a table runs Alg. 1's loop literally (one
+                               block-wide argmax per commit).  Read by TAPER_POLICY_GREEDY
+                               only.  Concave = fairness, weighted = priority (L142).   */
   int32_t ctx_counting;     /* taper_ctx_counting (0 = the paper's per-sequence count) */
+  int32_t utility_stride;   /* columns of `utility` (>= 2 when utility != NULL)         */
 } taper_policy;
 
 /* Batch state, structure-of-arrays (device).  Request r's ready slots are the slot
@@ -152,7 +160,7 @@ TAPER_API int taper_workspace_size(int32_t n_req, int32_t n_slot, int32_t h_loca
  * Greedy with linear utility is evaluated as a sort of candidates by (dL, r, slot)
  * followed by a prefix scan and the budget predicate on T(n0+m, L0+S_m); see DESIGN.md
  * for why this equals Alg. 1 bit for bit.  fp64, IEEE round-to-nearest, no FMA.
- * Errors: TAPER_ERR_ARG, _RHO, _NONMONOTONE, _CAPACITY, _UNSUPPORTED, _CUDA.           */
+ * Errors: TAPER_ERR_ARG, _RHO, _NONMONOTONE, _CAPACITY, _CUDA.                         */
 TAPER_API int taper_admit(const taper_batch *batch, const taper_latency_model *model,
                 const taper_policy *policy, const taper_admission *out, int32_t h_local,
                 void *workspace, size_t workspace_bytes, void *stream);

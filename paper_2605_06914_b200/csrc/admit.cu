@@ -19,6 +19,7 @@ namespace taper {
 
 constexpr int kAdmitThreads = 1024;
 constexpr int kPerThread = kMaxSlots / kAdmitThreads;  // 4
+constexpr double kEps = 1e-9;  // Alg. 1 line 16 "EPS" (no value in the paper) [C-adm-3]
 
 struct AdmitParams {
   int R, S;
@@ -27,6 +28,8 @@ struct AdmitParams {
   double a, b, c, rho;
   int kind, cap;
   int ctx_per_request;  // TAPER_CTX_PER_REQUEST: an opportunistic slot adds Lloc only
+  const double *util;   // [R][ustride] u_r(k) (flat past the table); NULL = linear
+  int ustride;
   int decide;  // 1: admission + work list; 0: work list from slot_admitted only
   int32_t *req_width;
   uint8_t *slot_admitted;
@@ -117,6 +120,117 @@ __device__ __forceinline__ double warp_min_d(double x) {
   return x;
 }
 
+// u_r(k) of the caller's table, flat past its last column (as the oracle reads it)
+__device__ __forceinline__ double util_at(const AdmitParams &p, int r, int k) {
+  return p.util[(long long)r * p.ustride + min(k, p.ustride - 1)];
+}
+
+// (score, r) lexicographic argmax: higher score, ties to the lower request index -- the
+// strict '>' of Alg. 1 line 18 scanned in ascending r [C-adm-4].  r < 0 = no candidate.
+struct Best { double score; long long dL; int r; };
+__device__ __forceinline__ bool better(double s1, int r1, double s2, int r2) {
+  if (r2 < 0) return r1 >= 0;
+  if (r1 < 0) return false;
+  return s1 > s2 || (s1 == s2 && r1 < r2);
+}
+__device__ __forceinline__ Best warp_argmax(Best b) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    Best o;
+    o.score = __shfl_xor_sync(0xffffffffu, b.score, d);
+    o.dL = __shfl_xor_sync(0xffffffffu, b.dL, d);
+    o.r = __shfl_xor_sync(0xffffffffu, b.r, d);
+    if (better(o.score, o.r, b.score, b.r)) b = o;
+  }
+  return b;
+}
+
+// Algorithm 1 executed literally for a caller-supplied utility
+// table (Sec. 3.4 "pluggable utility interface").  keys[] holds
+// the opportunistic slots sorted request-major (r, Lloc, slot), so request r's next
+// branch in canonical order [C-adm-1] is keys[start_r + granted_r].  One iteration of
+// the while-loop (L158-178): every live request evaluates its candidate in fp64 exactly
+// as the oracle does (T(n+1, L+dL) against the budget -> prune; du / (EPS + max(0, dt))),
+// a block-wide argmax picks the commit, and every thread applies it to (n, L).  One named
+// barrier per iteration (the per-warp winners are double-buffered by iteration parity).
+// Only the first ceil(R / 32) warps (<= 32) take part; thread t owns requests t, t + T, ..
+__device__ void greedy_literal(const AdmitParams &p, const unsigned long long *keys,
+                               int *scan_i, long long n0, long long L0, double budget,
+                               long long *nadd_out, long long *Ladd_out) {
+  constexpr int kOwn = kMaxSlots / kAdmitThreads;  // 4 requests per thread at most
+  __shared__ double wb_score[2][32];
+  __shared__ long long wb_dL[2][32];
+  __shared__ int wb_r[2][32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int R = p.R;
+  // start_r: exclusive scan of the opportunistic counts, request-major like the keys
+  int cnt[kPerThread];
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) {
+    int r = tid * kPerThread + k;
+    cnt[k] = (r < R) ? max(0, p.off[r + 1] - p.off[r] - 1) : 0;
+  }
+  block_exscan4<int>(cnt, scan_i);
+#pragma unroll
+  for (int k = 0; k < kPerThread; ++k) {
+    int r = tid * kPerThread + k;
+    if (r < R) p.req_part_off[r] = cnt[k];  // scratch: rewritten by the work-list pass
+  }
+  __syncthreads();
+  const int nwarps = min(kAdmitThreads / 32, max(1, (R + 31) / 32));
+  const int nthr = nwarps * 32;
+  if (tid < nthr) {
+    int start[kOwn], count[kOwn], g[kOwn];
+    long long lsh[kOwn];
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k) {
+      const int r = tid + k * nthr;
+      start[k] = 0; count[k] = 0; g[k] = 0; lsh[k] = 0;
+      if (r < R) {
+        start[k] = p.req_part_off[r];
+        count[k] = max(0, p.off[r + 1] - p.off[r] - 1);
+        lsh[k] = p.ctx_per_request ? 0ll : (long long)p.Lsh[r];
+      }
+    }
+    long long n = n0, L = L0;
+    for (int it = 0;; ++it) {
+      Best b{0.0, 0, -1};
+      const double T_step = T_eval(p.a, p.b, p.c, n, L);
+#pragma unroll
+      for (int k = 0; k < kOwn; ++k) {
+        if (g[k] >= count[k]) continue;  // exhausted or pruned (count forced to g)
+        const int r = tid + k * nthr;
+        const int s = int(keys[start[k] + g[k]] & 0xFFF);
+        const long long dL = lsh[k] + (long long)p.Lloc[s];
+        const double T_widened = T_eval(p.a, p.b, p.c, n + 1, L + dL);
+        if (T_widened > budget) { count[k] = g[k]; continue; }  // L164: prune r
+        const double du = __dsub_rn(util_at(p, r, g[k] + 1), util_at(p, r, g[k]));
+        const double dt = __dsub_rn(T_widened, T_step);
+        const double score = __ddiv_rn(du, __dadd_rn(kEps, dt > 0.0 ? dt : 0.0));
+        if (better(score, r, b.score, b.r)) { b.score = score; b.dL = dL; b.r = r; }
+      }
+      b = warp_argmax(b);
+      const int buf = it & 1;
+      if (lane == 0) { wb_score[buf][tid >> 5] = b.score; wb_dL[buf][tid >> 5] = b.dL; wb_r[buf][tid >> 5] = b.r; }
+      asm volatile("bar.sync 1, %0;" :: "r"(nthr) : "memory");
+      Best w{0.0, 0, -1};
+      if (lane < nwarps) { w.score = wb_score[buf][lane]; w.dL = wb_dL[buf][lane]; w.r = wb_r[buf][lane]; }
+      w = warp_argmax(w);
+      if (w.r < 0 || w.score <= 0.0) break;  // L21-22: no feasible increment of value
+      n += 1; L += w.dL;                         // L23-26: commit
+#pragma unroll
+      for (int k = 0; k < kOwn; ++k)
+        if (tid + k * nthr == w.r) g[k] += 1;    // owner advances r (drops it when exhausted)
+    }
+    // admitted opportunistic slots: the first g_r of r's canonical run
+#pragma unroll
+    for (int k = 0; k < kOwn; ++k)
+      for (int j = 0; j < g[k]; ++j) p.slot_admitted[int(keys[start[k] + j] & 0xFFF)] = 1;
+    if (tid == 0) { *nadd_out = n - n0; *Ladd_out = L - L0; }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) {
   __shared__ unsigned long long keys[kMaxSlots];
   __shared__ long long scan_ll[33];
@@ -174,7 +288,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
         double B = residual > 0.0 ? residual : 0.0;
         budget = __dadd_rn(T0, __dmul_rn(p.rho, B));
       }
-      if (p.kind == TAPER_POLICY_GREEDY && p.c < __dmul_rn(budget, 0x1p-46))
+      if (p.kind == TAPER_POLICY_GREEDY && !p.util && p.c < __dmul_rn(budget, 0x1p-46))
         atomicOr(&sh_status, TAPER_STATUS_PRECISION);
       sh_n0 = n0; sh_L0 = L0; sh_T0 = T0; sh_budget = budget; sh_ms = ms;
       sh_nadd = 0; sh_Ladd = 0;
@@ -189,6 +303,9 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       int n_keys = 1;
       while (n_keys < S) n_keys <<= 1;
       const bool sorted_policy = p.kind == TAPER_POLICY_CAP || p.kind == TAPER_POLICY_GREEDY;
+      // request-major keys (r, Lloc, slot): each request's opportunistic slots form one
+      // run in canonical order (IRP-Ck, and Alg. 1 with a non-linear utility)
+      const bool request_major = p.kind == TAPER_POLICY_CAP || p.util != nullptr;
       long long my_nadd = 0, my_Ladd = 0;
       for (int s = tid; s < n_keys; s += blockDim.x) {
         unsigned long long key = ~0ull;
@@ -203,7 +320,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
             long long dL = (p.ctx_per_request ? 0ll : (long long)p.Lsh[r]) + (long long)p.Lloc[s];
             if (p.kind == TAPER_POLICY_EAGER) {
               adm = 1; my_nadd += 1; my_Ladd += dL;
-            } else if (p.kind == TAPER_POLICY_CAP) {
+            } else if (request_major) {
               key = ((unsigned long long)r << 43) | ((unsigned long long)p.Lloc[s] << 12) |
                     (unsigned long long)s;
             } else if (p.kind == TAPER_POLICY_GREEDY) {
@@ -234,6 +351,11 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
               my_Ladd += (p.ctx_per_request ? 0ll : (long long)p.Lsh[r]) + (long long)p.Lloc[s];
             }
           }
+        } else if (request_major) {
+          // GREEDY, non-linear utility: Alg. 1 literally (scores differ per request, so
+          // the commit order is no longer a fixed sort of the candidates)
+          greedy_literal(p, keys, scan_i, sh_n0, sh_L0, sh_budget, &sh_nadd, &sh_Ladd);
+          my_nadd = 0; my_Ladd = 0;
         } else {
           // GREEDY: inclusive prefix sums of dL over the sorted candidates
           const int ncand = sh_ncand;
@@ -449,7 +571,11 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
         unsigned long long key = ~0ull;
         if (i < D) {
           const ItemDesc d = p.items[i];
-          const int cost = d.nt * (d.w > 4 ? 3 : 2);
+          // the branch groups of one prefix chunk (w_r > 8) share the cost of the widest
+          // group, so they stay adjacent in the claim order: claimed together, the later
+          // group re-reads the chunk from L2 instead of HBM
+          const int wr = (d.flags & 1) ? d.w : p.req_adm_off[d.r + 1] - p.req_adm_off[d.r];
+          const int cost = d.nt * (min(wr, kMaxItemBranches) > 4 ? 3 : 2);
           key = ((unsigned long long)(0xffff - cost) << 32) | (unsigned)i;
         }
         keys[i] = key;
@@ -510,8 +636,13 @@ static int launch_admit(const taper_batch *batch, const taper_latency_model *mod
     if (policy->kind < TAPER_POLICY_OFF || policy->kind > TAPER_POLICY_GREEDY)
       return fail(TAPER_ERR_ARG, "unknown policy kind");
     if (policy->kind == TAPER_POLICY_CAP && policy->cap < 1) return fail(TAPER_ERR_ARG, "cap must be >= 1");
-    if (policy->marginal_utility)
-      return fail(TAPER_ERR_UNSUPPORTED, "only linear utility is implemented on the device");
+    if (policy->utility && policy->utility_stride < 2)
+      return fail(TAPER_ERR_ARG, "utility_stride must be >= 2 when a utility table is given");
+    // the utility curve matters to Alg. 1 only; the fixed policies ignore it (App. D)
+    if (policy->kind == TAPER_POLICY_GREEDY && policy->utility) {
+      p.util = policy->utility;
+      p.ustride = policy->utility_stride;
+    }
     p.a = model->a; p.b = model->b; p.c = model->c; p.rho = policy->rho;
     p.kind = policy->kind; p.cap = policy->cap;
     if (policy->ctx_counting != TAPER_CTX_PER_SEQUENCE && policy->ctx_counting != TAPER_CTX_PER_REQUEST)

@@ -31,7 +31,7 @@ extern "C" const char *taper_status_string(int code) {
     case TAPER_ERR_NONMONOTONE: return "latency model not monotone (need a >= 0, b > 0, c > 0)";
     case TAPER_ERR_CAPACITY: return "capacity exceeded (slots, page size or workspace)";
     case TAPER_ERR_CUDA: return "CUDA error";
-    case TAPER_ERR_UNSUPPORTED: return "unsupported (non-linear utility on device)";
+    case TAPER_ERR_UNSUPPORTED: return "unsupported";
     default: break;
   }
   if (code > 0) {

@@ -36,7 +36,8 @@ class _Model(ctypes.Structure):
 
 class _Policy(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("cap", ctypes.c_int32), ("rho", ctypes.c_double),
-                ("marginal_utility", _vp), ("ctx_counting", ctypes.c_int32)]
+                ("utility", _vp), ("ctx_counting", ctypes.c_int32),
+                ("utility_stride", ctypes.c_int32)]
 
 
 CTX_COUNTING = {"per_sequence": 0, "per_request": 1}
@@ -234,12 +235,21 @@ def taper_workspace_size(n_req: int, n_slot: int, h_local: int, max_chunk_slots:
 
 def taper_admit(batch: DeviceBatch, model, policy: str = "taper", rho: float = 0.8,
                 adm: DeviceAdmission = None, h_local: int = 8, workspace: torch.Tensor = None,
-                cap: int = 2, stream=None, ctx: str = "per_sequence") -> DeviceAdmission:
+                cap: int = 2, stream=None, ctx: str = "per_sequence",
+                utility: torch.Tensor | None = None) -> DeviceAdmission:
+    """utility: None (linear u_r(k) = k) or a float64 device tensor [R, K] with
+    utility[r, k] = u_r(k), flat past column K-1 (include/taper.h taper_policy)."""
     a, b, c = (float(x) for x in model)
+    ustride = 0
+    if utility is not None:
+        assert utility.dtype == torch.float64 and utility.is_cuda and utility.is_contiguous()
+        assert utility.dim() == 2 and utility.shape[0] >= batch.n_req
+        ustride = utility.shape[1]
     kind = POLICY[policy] if isinstance(policy, str) else int(policy)
     bc, ac = batch.c(), adm.c()
     _check(_lib.taper_admit(ctypes.byref(bc), ctypes.byref(_Model(a, b, c)),
-                            ctypes.byref(_Policy(kind, cap, rho, None, CTX_COUNTING[ctx])),
+                            ctypes.byref(_Policy(kind, cap, rho, _ptr(utility), CTX_COUNTING[ctx],
+                                                 ustride)),
                             ctypes.byref(ac),
                             h_local, _ptr(workspace), workspace.numel() * workspace.element_size(),
                             _stream(stream)), "taper_admit")

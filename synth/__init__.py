@@ -291,3 +291,26 @@ class TraceReplay:
                     self.lsh[r] += sum(self._finished.pop(r))
                     self.serial_left[r] = int(self.rng.integers(16, 129))
         self.step_idx += 1
+
+
+def utility_table(rng, R: int, K: int, kind: str = "concave") -> np.ndarray:
+    """Operator-supplied utility curves u_r(k), k = 0..K-1 (Sec. 3.4), as a float64
+    [R, K] table with u_r(0) = 0 and non-decreasing columns.  Kinds (input shapes only):
+      linear   u_r(k) = k (the paper's default)
+      weighted u_r(k) = w_r k, w_r in {1, 2, 5, 10} ("priority operators weight by tenant")
+      concave  increments non-increasing in k ("the first opportunistic branch matters more")
+      plateau  concave, with zero increments after a random k (a request that wants no more)
+    """
+    k = np.arange(K, dtype=np.float64)
+    if kind == "linear":
+        return np.tile(k, (R, 1))
+    if kind == "weighted":
+        w = rng.choice([1.0, 2.0, 5.0, 10.0], size=R)
+        return w[:, None] * k[None, :]
+    inc = np.sort(rng.uniform(0.05, 4.0, size=(R, K - 1)), axis=1)[:, ::-1]
+    if kind == "plateau":
+        stop = rng.integers(0, K, size=R)
+        inc = np.where(np.arange(K - 1)[None, :] >= stop[:, None], 0.0, inc)
+    elif kind != "concave":
+        raise ValueError(kind)
+    return np.concatenate([np.zeros((R, 1)), np.cumsum(inc, axis=1)], axis=1)

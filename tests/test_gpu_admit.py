@@ -10,22 +10,23 @@ import synth
 pytestmark = pytest.mark.gpu
 
 
-def _gpu_admit(b, model, policy, rho, cap=2, h=8, ctx="per_sequence"):
+def _gpu_admit(b, model, policy, rho, cap=2, h=8, ctx="per_sequence", utility=None):
     from paper_2605_06914_b200 import taper as T
     db = T.DeviceBatch.from_host(b)
     adm = T.DeviceAdmission.empty(b.n_req, b.n_slot)
     ws = torch.empty(T.taper_workspace_size(b.n_req, b.n_slot, h,
                                             T.max_chunk_slots(b.req_shared_len, b.req_slot_off, b.slot_local_len)),
                      dtype=torch.uint8, device="cuda")
-    T.taper_admit(db, model, policy, rho, adm, h, ws, cap, ctx=ctx)
+    u = None if utility is None else torch.as_tensor(utility, dtype=torch.float64).cuda()
+    T.taper_admit(db, model, policy, rho, adm, h, ws, cap, ctx=ctx, utility=u)
     torch.cuda.synchronize()
     return adm
 
 
-def _compare(b, model, policy, rho, cap=2, ctx="per_sequence"):
-    g = _gpu_admit(b, model, policy, rho, cap, ctx=ctx)
+def _compare(b, model, policy, rho, cap=2, ctx="per_sequence", utility=None):
+    g = _gpu_admit(b, model, policy, rho, cap, ctx=ctx, utility=utility)
     o = oracle.admit(b.req_shared_len, b.req_slot_off, b.req_slack_ms, b.slot_local_len, model,
-                     policy, cap, rho, ctx=ctx)
+                     policy, cap, rho, utility=utility, ctx=ctx)
     R, S = b.n_req, b.n_slot
     np.testing.assert_array_equal(g.req_width.cpu().numpy()[:R], o.req_width)
     np.testing.assert_array_equal(g.slot_admitted.cpu().numpy()[:S], o.slot_admitted)
@@ -106,3 +107,64 @@ def test_invalid_arguments_rejected():
         _gpu_admit(b, (1.0, 0.0, 0.01), "taper", 0.8)
     with pytest.raises(T.TaperError, match="monotone"):
         _gpu_admit(b, (1.0, 0.1, -1.0), "taper", 0.8)
+
+
+# ---------------------------------------------------------------- non-linear utilities
+# Sec. 3.4 (L142) "pluggable utility interface"; Alg. 1 line 15 (L167).  The device runs
+# Alg. 1's loop literally for a utility table; it must match the literal oracle bit for bit.
+
+@pytest.mark.parametrize("ctx", ["per_sequence", "per_request"])
+@pytest.mark.parametrize("kind", ["concave", "weighted", "plateau", "linear"])
+def test_utility_tables_match_oracle(kind, ctx):
+    rng = np.random.default_rng(7)
+    for i in range(200):
+        b = synth.random_small_batch(rng, max_req=14, max_fanout=7, max_local=50)
+        K = int(rng.integers(2, 9))  # short tables exercise the flat extension
+        util = synth.utility_table(rng, b.n_req, K, kind)
+        model = (rng.uniform(0, 20), rng.uniform(1e-3, 0.1), rng.uniform(1e-5, 1e-2))
+        _compare(b, model, "taper", float(rng.uniform(0.05, 1.0)), ctx=ctx, utility=util)
+
+
+def test_linear_table_equals_sort_scan_path():
+    """u_r(k) = k as a table (literal loop on the device) == utility=NULL (sort + scan):
+    two device formulations of Alg. 1 that share no code past the candidate keys."""
+    rng = np.random.default_rng(11)
+    for name in ("c2", "c5"):
+        b = synth.config_batch(name, seed=2, slack_min_ms=0.0)
+        b.req_slack_ms = 40.0 + rng.uniform(0, 20, size=b.n_req)
+        K = int(np.diff(b.req_slot_off).max()) + 1
+        lin = synth.utility_table(rng, b.n_req, K, "linear")
+        for rho in (0.2, 0.5, 0.8, 1.0):
+            g1 = _gpu_admit(b, (12.0, 0.03, 2e-5), "taper", rho, utility=lin)
+            g2 = _gpu_admit(b, (12.0, 0.03, 2e-5), "taper", rho)
+            assert torch.equal(g1.slot_admitted, g2.slot_admitted)
+            assert g1.diag.cpu().numpy().tobytes() == g2.diag.cpu().numpy().tobytes()
+
+
+@pytest.mark.parametrize("kind", ["concave", "weighted"])
+def test_utility_config_batches(kind):
+    """Config-sized batches (c2: 64 requests; c5: 256 requests, ~390 candidates), every
+    regime of the budget, bit-exact against the literal oracle."""
+    rng = np.random.default_rng(13)
+    for name in ("c2", "c5"):
+        b = synth.config_batch(name, seed=4, slack_min_ms=0.0)
+        util = synth.utility_table(rng, b.n_req, 17, kind)
+        for base in (10.0, 30.0, 45.0, 80.0):
+            b.req_slack_ms = base + rng.uniform(0, 20, size=b.n_req)
+            _compare(b, (12.0, 0.03, 2e-5), "taper", 0.8, utility=util)
+
+
+def test_utility_max_capacity():
+    rng = np.random.default_rng(17)
+    fan = np.full(1024, 4)
+    b = synth.make_batch(rng.integers(0, 32768, 1024), fan, rng.integers(0, 512, 4096), 40.0, 20.0,
+                         rng=rng)
+    util = synth.utility_table(rng, b.n_req, 4, "concave")
+    _compare(b, (12.0, 0.03, 2e-5), "taper", 0.8, utility=util)
+
+
+def test_utility_stride_validated():
+    from paper_2605_06914_b200 import taper as T
+    b = synth.config_batch("c1")
+    with pytest.raises(T.TaperError, match="utility_stride"):
+        _gpu_admit(b, (1.0, 0.1, 0.01), "taper", 0.8, utility=np.zeros((b.n_req, 1)))

@@ -310,3 +310,30 @@ def test_per_request_greedy_is_optimal_and_dominates():
         assert req.req_width.sum() - b.n_req == best
         assert req.T_S <= budget
         assert np.all(req.slot_admitted >= seq.slot_admitted)
+
+
+@pytest.mark.parametrize("kind", ["concave", "weighted", "plateau"])
+def test_nonlinear_utility_greedy_feasible_and_bounded_by_optimum(kind):
+    """App. B (L290-305) with operator utilities (L142): the literal Alg. 1 must return a
+    feasible allocation (T(S) <= budget, progress for every request) whose utility never
+    exceeds the exhaustive optimum.  The ratio greedy / optimum is reported, not asserted
+    >= 1/2: the Remark's factor does not hold for plain density greedy [C-adm-12]."""
+    rng = np.random.default_rng(23)
+    ratios = []
+    for _ in range(300):
+        b = synth.random_small_batch(rng, max_req=5, max_fanout=4, max_local=40)
+        if b.n_slot - b.n_req > 14:
+            continue
+        util = synth.utility_table(rng, b.n_req, 4, kind)
+        model = (rng.uniform(0, 5), rng.uniform(1e-2, 0.5), rng.uniform(1e-4, 1e-2))
+        rho = float(rng.uniform(0.1, 1.0))
+        g = _admit(b, model, rho=rho, utility=util)
+        best, _, _, budget = oracle.bruteforce(b.req_shared_len, b.req_slot_off, b.req_slack_ms,
+                                               b.slot_local_len, model, rho, util)
+        assert g.T_S <= g.budget and g.budget == budget
+        assert (g.req_width >= 1).all()
+        got = sum(util[r, min(int(g.req_width[r]) - 1, util.shape[1] - 1)] for r in range(b.n_req))
+        assert got <= best + 1e-9
+        if best > 0:
+            ratios.append(got / best)
+    assert len(ratios) > 40 and min(ratios) > 0.0
