@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--slack-x", type=float, default=2.0,
                     help="min slack = T0 + x (T_eager - T0)/rho; x >= 1 admits every branch")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--rank-of", type=int, default=0, metavar="G",
+                    help="single GPU only: run the per-rank work of a G-GPU KV-head shard "
+                         "(8/G heads, no collectives) -- what one rank of G does")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -245,6 +248,9 @@ def run_ours(args):
     G = world
     assert 8 % G == 0, "KV heads (8) must divide evenly across GPUs"
     h = 8 // G
+    if args.rank_of:
+        assert G == 1 and 8 % args.rank_of == 0, "--rank-of emulates one rank on one GPU"
+        h = 8 // args.rank_of
     L = args.layers
     batch = build_batch(args)
     R, S = batch.n_req, batch.n_slot
@@ -399,7 +405,10 @@ def run_ours(args):
                 "slack_x": args.slack_x, "admitted_slots": int(adm_mask.sum()),
                 "ready_slots": S, "requests": R, "layers": L,
                 "kv_layer_buffers": n_distinct,
-                "kv_heads_per_gpu": h, "parallelism": f"kv-head shard x{G}",
+                "kv_heads_per_gpu": h,
+                "parallelism": (f"kv-head shard x{G}" if not args.rank_of else
+                                f"one rank of a kv-head shard x{args.rank_of} (per-rank work, "
+                                "no collectives; value = that rank's steps/s)"),
                 "l2": f"inputs larger than L2 ({layer_bytes / 1e9:.2f} GB K/V per layer per GPU)",
                 "step": "admit + 64 x decode_attention (+ bcast/all-gather when G>1); no FFN",
             },

@@ -119,6 +119,16 @@ typedef struct {
   const double *req_slack_ms;     /* [R]   d_r(t) - t in ms (L130)                      */
   const int32_t *slot_local_len;  /* [S]   Lloc_s: branch-local tokens h_i (+) y_{i,<=t},
                                      the current token already appended (0 for serial) */
+  /* Optional multi-segment local context (NULL = one segment of Lloc_s tokens per slot).
+   * Sec. 3.1 (L104-107): at a reduce step the context is P (+) H (+) every branch's
+   * h_i (+) y_i in canonical order (+) z -- a concatenation of segments that already sit
+   * in the cache in their own pages.  Slot s's local context is then its segments
+   * [slot_seg_off[s], slot_seg_off[s+1]) in order, each starting on a page boundary
+   * (taper_kv.seg_page_off), so a reduce step reads the branches' KV where it lies
+   * instead of copying it.  sum of slot s's seg_len == slot_local_len[s], else
+   * TAPER_STATUS_BAD_LENGTH.                                                          */
+  const int32_t *slot_seg_off;    /* [S+1] CSR over slots, or NULL                      */
+  const int32_t *seg_len;         /* [n_seg] tokens of each local segment (>= 0)        */
 } taper_batch;
 
 /* Admission outputs (device, caller-allocated).                                         */
@@ -144,12 +154,17 @@ typedef struct {
                                   req_pages[req_page_off[r] + t / page_size]            */
   const int32_t *slot_page_off; /* [S+1] CSR: pages of slot s's local segment          */
   const int32_t *slot_pages;
+  const int32_t *seg_page_off;  /* [n_seg] with taper_batch.slot_seg_off: token t of local
+                                   segment q is row t % page_size of page
+                                   slot_pages[seg_page_off[q] + t / page_size]
+                                   (slot_page_off is then unused); else NULL            */
 } taper_kv;
 
 /* Workspace bytes for a batch of at most n_req requests / n_slot slots on a rank with
  * h_local KV heads.  max_chunk_slots bounds the partial rows' count
  *     sum_r w_r * ceil(Lsh_r / TAPER_CHUNK_TOKENS)  +  sum_{s admitted} ceil(Lloc_s / 1024)
- * (prefix chunks per admitted branch, plus one per local item of <= 16 64-token tiles);
+ * (prefix chunks per admitted branch, plus one per local item of <= 16 64-token tiles;
+ * with local segments the second sum runs over segments: sum ceil(seg_len / 1024));
  * the Eager value of that sum over all ready slots is always enough.  An undersized
  * workspace is reported as TAPER_STATUS_WORK_OVERFLOW, never overrun.  [host]           */
 TAPER_API int taper_workspace_size(int32_t n_req, int32_t n_slot, int32_t h_local,

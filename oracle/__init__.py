@@ -70,6 +70,9 @@ def _load():
         lib.oracle_attention.restype = ctypes.c_int
         lib.oracle_attention.argtypes = [i32, P, i32, i32, i32, i32, P, P, P, P, P, P, P, P,
                                          P, i32, P, P, f64, P, P]
+        lib.oracle_attention_seg.restype = ctypes.c_int
+        lib.oracle_attention_seg.argtypes = [i32, P, i32, i32, i32, i32, P, P, P, P, P, P, P, P,
+                                             P, P, P, P, i32, P, P, f64, P, P]
         _lib = lib
     return _lib
 
@@ -159,9 +162,12 @@ def bruteforce(req_shared_len, req_slot_off, req_slack_ms, slot_local_len, model
 
 def attention(req_slot_off, req_shared_len, slot_local_len, req_page_off, req_pages,
               slot_page_off, slot_pages, k_pages, v_pages, q, eval_slot, eval_qhead,
-              scale=None):
+              scale=None, slot_seg_off=None, seg_len=None, seg_page_off=None):
     """Sec. 3.1 visibility rule (L100-103): fp64 softmax attention of (slot, q-head)
-    pairs over the materialised [shared prefix ; branch-local] context.
+    pairs over the materialised [shared prefix ; branch-local] context.  With
+    ``slot_seg_off`` the local context is the concatenation of the slot's segments
+    (reduce step, L104-107), segment q holding ``seg_len[q]`` tokens in the page list
+    starting at ``slot_pages[seg_page_off[q]]``.
 
     k_pages/v_pages: [num_pages, h_kv, page, d] bf16 (uint16 bit patterns or torch bf16).
     q: [S, q_heads, d] bf16 bits.  Returns (out [n, d] fp64, lse [n] fp64, natural log).
@@ -178,12 +184,14 @@ def attention(req_slot_off, req_shared_len, slot_local_len, req_page_off, req_pa
     out = np.zeros((n, d), np.float64)
     lse = np.zeros(n, np.float64)
     off = _i32(req_slot_off)
-    st = _load().oracle_attention(len(off) - 1, _p(off), h_kv, q_heads, d, page_size,
-                                  _p(k_bits), _p(v_bits), _p(_i32(req_shared_len)),
-                                  _p(_i32(req_page_off)), _p(_i32(req_pages)),
-                                  _p(_i32(slot_local_len)), _p(_i32(slot_page_off)),
-                                  _p(_i32(slot_pages)), _p(q_bits), n, _p(es), _p(eh),
-                                  float(scale), _p(out), _p(lse))
+    seg = [None, None, None] if slot_seg_off is None else \
+        [_i32(slot_seg_off), _i32(seg_len), _i32(seg_page_off)]
+    st = _load().oracle_attention_seg(len(off) - 1, _p(off), h_kv, q_heads, d, page_size,
+                                      _p(k_bits), _p(v_bits), _p(_i32(req_shared_len)),
+                                      _p(_i32(req_page_off)), _p(_i32(req_pages)),
+                                      _p(_i32(slot_local_len)), _p(_i32(slot_page_off)),
+                                      _p(_i32(slot_pages)), *[_p(a) for a in seg], _p(q_bits),
+                                      n, _p(es), _p(eh), float(scale), _p(out), _p(lse))
     if st < 0:
         raise ValueError(f"oracle_attention error {st}")
     return out, lse

@@ -23,7 +23,8 @@
  *                       softmax attention in fp64 over the fully materialised
  *                       per-branch context [shared prefix ; branch-local]
  *                       (prefix duplicated per branch), one (slot, q-head) at
- *                       a time.
+ *                       a time.  oracle_attention_seg: the local context may be
+ *                       several segments (reduce step, L104-107).
  *
  * Readings of the paper where it is silent are listed in DESIGN.md
  * ("Readings"); the ones used here are tagged [C-adm-n] / [C-att-n].
@@ -320,25 +321,31 @@ static double bf16_to_double(uint16_t h) {
 }
 
 /*
- * oracle_attention: plain fp64 softmax attention for selected (slot, q-head)
+ * oracle_attention_seg: plain fp64 softmax attention for selected (slot, q-head)
  * pairs.  KV pages: [num_pages][h_kv][page_size][d] bf16 (bit patterns).
  * Token t of a segment with page list P lives in page P[t / page_size] at
- * row t % page_size.  Slot s of request r sees
+ * row t % page_size.  Slot s of request r sees the concatenation
  *     K = [K_shared(r) tokens 0..Lsh[r]-1 ; K_local(s) tokens 0..Lloc[s]-1]
  * (visibility rule, Sec. 3.1; current token already appended
- * [C-att-3]).  Q head hq reads KV head hq / (q_heads / h_kv) [C-att-2].
+ * [C-att-3]).  The local context is one segment (page list slot_pages from
+ * slot_page_off[s]) or, when slot_seg_off != NULL, the segments
+ * slot_seg_off[s] .. slot_seg_off[s+1]-1 in order, segment q holding seg_len[q]
+ * tokens in the page list slot_pages from seg_page_off[q] -- the reduce-step
+ * context P (+) H (+) h_1 (+) y_1 (+) ... (+) z of Sec. 3.1 (L104-107).
+ * Q head hq reads KV head hq / (q_heads / h_kv) [C-att-2].
  *   x_j = scale * q . k_j ;  p = softmax(x) ;  o = sum_j p_j v_j
  *   lse = log(sum_j exp(x_j))   (natural log)
  * q: [S][q_heads][d] bf16 bits.  out: [n_eval][d], lse: [n_eval].
  */
-int oracle_attention(int32_t R, const int32_t *off, int32_t h_kv, int32_t q_heads,
-                     int32_t d, int32_t page_size, const uint16_t *k_pages,
-                     const uint16_t *v_pages, const int32_t *Lsh,
-                     const int32_t *req_page_off, const int32_t *req_pages,
-                     const int32_t *Lloc, const int32_t *slot_page_off,
-                     const int32_t *slot_pages, const uint16_t *q, int32_t n_eval,
-                     const int32_t *eval_slot, const int32_t *eval_qhead, double scale,
-                     double *out, double *lse) {
+int oracle_attention_seg(int32_t R, const int32_t *off, int32_t h_kv, int32_t q_heads,
+                         int32_t d, int32_t page_size, const uint16_t *k_pages,
+                         const uint16_t *v_pages, const int32_t *Lsh,
+                         const int32_t *req_page_off, const int32_t *req_pages,
+                         const int32_t *Lloc, const int32_t *slot_page_off,
+                         const int32_t *slot_pages, const int32_t *slot_seg_off,
+                         const int32_t *seg_len, const int32_t *seg_page_off,
+                         const uint16_t *q, int32_t n_eval, const int32_t *eval_slot,
+                         const int32_t *eval_qhead, double scale, double *out, double *lse) {
   if (h_kv <= 0 || q_heads % h_kv != 0 || d <= 0 || page_size <= 0) return ORACLE_ERR_ARG;
   int32_t group = q_heads / h_kv;
   for (int32_t e = 0; e < n_eval; ++e) {
@@ -352,6 +359,11 @@ int oracle_attention(int32_t R, const int32_t *off, int32_t h_kv, int32_t q_head
     if (r < 0) return ORACLE_ERR_ARG;
     int64_t n_sh = Lsh[r], n_loc = Lloc[s], n_tok = n_sh + n_loc;
     if (n_tok < 1) return ORACLE_ERR_ARG; /* [C-att-4] */
+    if (slot_seg_off) { /* the segments must make up the local context exactly */
+      int64_t sum = 0;
+      for (int32_t qs = slot_seg_off[s]; qs < slot_seg_off[s + 1]; ++qs) sum += seg_len[qs];
+      if (sum != n_loc) return ORACLE_ERR_ARG;
+    }
     /* Materialise this branch's K and V (prefix duplicated per branch). */
     double *K = (double *)malloc(sizeof(double) * (size_t)(n_tok * d));
     double *V = (double *)malloc(sizeof(double) * (size_t)(n_tok * d));
@@ -360,9 +372,16 @@ int oracle_attention(int32_t R, const int32_t *off, int32_t h_kv, int32_t q_head
       if (t < n_sh) {
         page = req_pages[req_page_off[r] + t / page_size];
         row = t % page_size;
-      } else {
+      } else if (!slot_seg_off) {
         int64_t u = t - n_sh;
         page = slot_pages[slot_page_off[s] + u / page_size];
+        row = u % page_size;
+      } else {
+        /* find the local segment holding local token u */
+        int64_t u = t - n_sh;
+        int32_t qs = slot_seg_off[s];
+        while (u >= seg_len[qs]) { u -= seg_len[qs]; ++qs; }
+        page = slot_pages[seg_page_off[qs] + u / page_size];
         row = u % page_size;
       }
       int64_t base = ((page * h_kv + g) * page_size + row) * d;
@@ -399,4 +418,18 @@ int oracle_attention(int32_t R, const int32_t *off, int32_t h_kv, int32_t q_head
     free(x);
   }
   return ORACLE_OK;
+}
+
+/* oracle_attention: oracle_attention_seg with one local segment per slot. */
+int oracle_attention(int32_t R, const int32_t *off, int32_t h_kv, int32_t q_heads,
+                     int32_t d, int32_t page_size, const uint16_t *k_pages,
+                     const uint16_t *v_pages, const int32_t *Lsh,
+                     const int32_t *req_page_off, const int32_t *req_pages,
+                     const int32_t *Lloc, const int32_t *slot_page_off,
+                     const int32_t *slot_pages, const uint16_t *q, int32_t n_eval,
+                     const int32_t *eval_slot, const int32_t *eval_qhead, double scale,
+                     double *out, double *lse) {
+  return oracle_attention_seg(R, off, h_kv, q_heads, d, page_size, k_pages, v_pages, Lsh,
+                              req_page_off, req_pages, Lloc, slot_page_off, slot_pages, NULL,
+                              NULL, NULL, q, n_eval, eval_slot, eval_qhead, scale, out, lse);
 }

@@ -24,6 +24,7 @@ constexpr double kEps = 1e-9;  // Alg. 1 line 16 "EPS" (no value in the paper) [
 struct AdmitParams {
   int R, S;
   const int32_t *Lsh, *off, *Lloc;
+  const int32_t *seg_off, *seg_len;  // local segments (CSR over S), or NULL = one per slot
   const double *slack;
   double a, b, c, rho;
   int kind, cap;
@@ -48,6 +49,16 @@ struct AdmitParams {
   int4 *ltiles;      // [cap_cs * 16] local tiles {slot, tok0, valid, jrow}
   int32_t *order;    // [cap_cs] claim order of the items (longest first)
 };
+
+// Local work items of slot s: one per <= kLocalItemTiles 64-token tiles of each of its
+// local segments (a tile never spans two segments: each starts on a page boundary).
+__device__ __forceinline__ int local_items(const AdmitParams &p, int s) {
+  constexpr int per = kTileTokens * kLocalItemTiles;
+  if (p.seg_off == nullptr) return (p.Lloc[s] + per - 1) / per;
+  int n = 0;
+  for (int q = p.seg_off[s]; q < p.seg_off[s + 1]; ++q) n += (max(p.seg_len[q], 0) + per - 1) / per;
+  return n;
+}
 
 __device__ __forceinline__ double T_eval(double a, double b, double c, long long n,
                                          long long L) {
@@ -259,6 +270,13 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       p.slot_req[s] = r;
       int l = p.Lloc[s];
       if (l < 0) atomicOr(&sh_status, TAPER_STATUS_BAD_LENGTH);
+      if (p.seg_off != nullptr) {  // segments must tile the local context exactly
+        const int q0 = p.seg_off[s], q1 = p.seg_off[s + 1];
+        long long sum = 0;
+        bool bad = q1 < q0;
+        for (int q = q0; q < q1 && !bad; ++q) { bad = p.seg_len[q] < 0; sum += p.seg_len[q]; }
+        if (bad || sum != l) atomicOr(&sh_status, TAPER_STATUS_BAD_LENGTH);
+      }
       if (prot < 0 || l < best) { prot = s; best = l; }  // canonical first (Lloc, slot)
     }
     if (p.decide) {
@@ -435,7 +453,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
         for (int s = b; s < e; ++s)
           if (p.slot_admitted[s]) {
             w += 1;
-            nl += (p.Lloc[s] + kTileTokens * kLocalItemTiles - 1) / (kTileTokens * kLocalItemTiles);
+            nl += local_items(p, s);
           }
         if (w > 0 && p.Lsh[r] > 0) nc = (p.Lsh[r] + kChunk - 1) / kChunk;
       }
@@ -509,21 +527,25 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     int li = 0;
     for (int j = 0; j < w; ++j) {
       const int s = p.adm_by_req[adm_off + j];
-      const int L = p.Lloc[s];
       p.slot_lbase[s] = li;  // local items of the request's branches before j
-      for (int t0 = 0; t0 < L; t0 += kTileTokens * kLocalItemTiles, ++li) {
-        const int nt = min(kLocalItemTiles, (L - t0 + kTileTokens - 1) / kTileTokens);
-        for (int t = 0; t < nt; ++t) {
-          const int tok = t0 + t * kTileTokens;
-          p.ltiles[(size_t)(l0 + li) * kLocalItemTiles + t] =
-              make_int4(s, tok, min(kTileTokens, L - tok), 0);
+      const int nseg = p.seg_off ? p.seg_off[s + 1] - p.seg_off[s] : 1;
+      for (int qs = 0; qs < nseg; ++qs) {
+        const int seg = p.seg_off ? p.seg_off[s] + qs : -1;  // -1: the slot's page list
+        const int L = p.seg_off ? p.seg_len[seg] : p.Lloc[s];
+        for (int t0 = 0; t0 < L; t0 += kTileTokens * kLocalItemTiles, ++li) {
+          const int nt = min(kLocalItemTiles, (L - t0 + kTileTokens - 1) / kTileTokens);
+          for (int t = 0; t < nt; ++t) {
+            const int tok = t0 + t * kTileTokens;
+            p.ltiles[(size_t)(l0 + li) * kLocalItemTiles + t] =
+                make_int4(s, tok, min(kTileTokens, L - tok), seg);
+          }
+          ItemDesc d;
+          d.r = r; d.w = 1; d.adm_off = adm_off + j; d.cs0 = cs_r + nc * w + li;
+          d.tb = (l0 + li) * kLocalItemTiles; d.te = 0;
+          d.nt = nt;
+          d.flags = 1;
+          p.items[it0 + nsh + li] = d;
         }
-        ItemDesc d;
-        d.r = r; d.w = 1; d.adm_off = adm_off + j; d.cs0 = cs_r + nc * w + li;
-        d.tb = (l0 + li) * kLocalItemTiles; d.te = 0;
-        d.nt = nt;
-        d.flags = 1;
-        p.items[it0 + nsh + li] = d;
       }
     }
   }
@@ -552,7 +574,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       const int n_items = (p.req_chunk_off[r + 1] - p.req_chunk_off[r]) +
                           (p.req_loc_off[r + 1] - p.req_loc_off[r]);
       const int lpre = p.slot_lbase[s];
-      const int nl = (p.Lloc[s] + kTileTokens * kLocalItemTiles - 1) / (kTileTokens * kLocalItemTiles);
+      const int nl = local_items(p, s);
       const int cs_r = p.req_part_off[r];
       p.merge_desc[2 * fl[k]] = make_int4(s, cs_r + j, nc, w);
       p.merge_desc[2 * fl[k] + 1] = make_int4(cs_r + nc * w + lpre, nl, r, n_items);
@@ -654,6 +676,8 @@ static int launch_admit(const taper_batch *batch, const taper_latency_model *mod
   char *w = static_cast<char *>(ws);
   p.R = R; p.S = S;
   p.Lsh = batch->req_shared_len; p.off = batch->req_slot_off; p.Lloc = batch->slot_local_len;
+  p.seg_off = batch->slot_seg_off; p.seg_len = batch->seg_len;
+  if (p.seg_off && !p.seg_len) return fail(TAPER_ERR_ARG, "slot_seg_off without seg_len");
   p.slack = batch->req_slack_ms;
   p.decide = decide;
   p.req_width = out->req_width; p.slot_admitted = out->slot_admitted;

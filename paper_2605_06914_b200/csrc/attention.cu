@@ -58,10 +58,15 @@ constexpr int kOffV = kKStages * kStageBytes;
 constexpr int kOffQ = kOffV + kVStages * kStageBytes;   // Q^T operand, 2 buffers x 64 rows
 constexpr int kQBytes = kMaxItemBranches * kGroup * 256;  // 16 KB: [branch][d-half][8][128 B]
 constexpr int kOffPT = kOffQ + 2 * kQBytes;              // P^T operand: 128 rows x 128 B
-constexpr int kPTBytes = 2 * kMaxItemBranches * kGroup * 128;
 // Items with <= 4 branches (P^T <= 8 KB) alternate between the two 8 KB halves by tile
 // parity, so softmax(n) only waits for PV(n-2); wider items use the whole buffer.
-constexpr int kNarrowPT = 4;
+#ifndef TAPER_NARROW_PT
+#define TAPER_NARROW_PT 4
+#endif
+constexpr int kNarrowPT = TAPER_NARROW_PT;
+constexpr int kPTHalf = 2 * kNarrowPT * kGroup * 128;  // hi + lo rows of kNarrowPT branches
+constexpr int kPTBytes = (2 * kPTHalf > 2 * kMaxItemBranches * kGroup * 128)
+                             ? 2 * kPTHalf : 2 * kMaxItemBranches * kGroup * 128;
 constexpr int kOffML = kOffPT + kPTBytes;  // (m, l) of the 64 stacked rows, 2 buffers
 // cross-warp reductions per softmax group: max [2 parities][4 warps][64], sum [4][64]
 constexpr int kRedFloats = 3 * 4 * 64;
@@ -73,6 +78,7 @@ constexpr int kOffRec = kOffAlpha + 8 * 64 * 4;
 constexpr int kOffBar = kOffRec + kItemRing * kRecBytes;
 constexpr int kSmemUsed = kOffBar + 512;
 constexpr int kSmemBytes = kSmemUsed + 1024;  // + alignment slack
+static_assert(kSmemBytes <= 232448, "exceeds 227 KB of dynamic SMEM per CTA");
 // warp 0: K producer; warp 1: MMA issuer; warps 2-5: softmax group 0; warps 6-9:
 // epilogue; warp 10: V producer; warp 11: item scheduler (claims, resolves tiles, loads Q);
 // warps 12-15: softmax group 1.  A group owns 8-row blocks of the stacked rows.
@@ -84,6 +90,7 @@ constexpr uint32_t kColO = 128;   // O^T 0 [128, 256), O^T 1 [256, 384): 128 d x
 
 struct AttnParams {
   const int32_t *slot_page_off, *slot_pages, *req_page_off, *req_pages;
+  const int32_t *seg_page_off;  // local segments' first page in slot_pages (NULL: unused)
   int32_t *hdr;        // hdr[8]: work counter, hdr[9]: CTAs exited
   const int32_t *adm_by_req;
   int32_t *done;       // [r * 8 + g]: items of (request, KV head) whose partials are written
@@ -138,8 +145,8 @@ __device__ __forceinline__ TileInfo tile_info(const AttnParams &p, const Item &x
     ti.tok0 = x.tb + t * kTile;
     ti.valid = min(kTile, x.te - ti.tok0);
   } else {
-    const int4 lt = __ldg(p.ltiles + x.tb + t);  // {slot, tok0, valid, -}
-    ti.pages = p.slot_pages + __ldg(p.slot_page_off + lt.x);
+    const int4 lt = __ldg(p.ltiles + x.tb + t);  // {slot, tok0, valid, segment or -1}
+    ti.pages = p.slot_pages + (lt.w >= 0 ? __ldg(p.seg_page_off + lt.w) : __ldg(p.slot_page_off + lt.x));
     ti.tok0 = lt.y;
     ti.valid = lt.z;
   }
@@ -477,7 +484,7 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
         tmem_st_wait();
       }
       if (C.warp == 2 && lane == 0) trace_ev(*C.p, 14, n);
-      const uint32_t pbuf = wide ? 0u : (n & 1) * (kPTBytes / 2);
+      const uint32_t pbuf = wide ? 0u : (n & 1) * kPTHalf;
 #pragma unroll
       for (int b = 0; b < WB; ++b)
         stmatrix_x4_trans(st_addr[b] + pbuf, pk[4 * b], pk[4 * b + 1], pk[4 * b + 2], pk[4 * b + 3]);
@@ -817,7 +824,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           tc_fence_after();
           if (elect_one()) {
             issue_pv(tO, sV + vs * kStageBytes,
-                     sPT + (wi > kNarrowPT ? 0u : (m & 1) * (kPTBytes / 2)), first, idesc_pv);
+                     sPT + (wi > kNarrowPT ? 0u : (m & 1) * kPTHalf), first, idesc_pv);
             tc_commit(vempty + vs);
             tc_commit(pv_done + (m & 1));
             if (t == nt) tc_commit(o_full + ob);
@@ -1188,6 +1195,8 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
        reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(TAPER_ERR_ARG, "K/V pools, q and out must be 16-byte aligned");
   if (!adm->adm_list || !adm->slot_admitted) return fail(TAPER_ERR_ARG, "null admission arrays");
+  if ((batch->slot_seg_off != nullptr) != (kv->seg_page_off != nullptr))
+    return fail(TAPER_ERR_ARG, "batch.slot_seg_off and kv.seg_page_off must be given together");
   WsLayout L = ws_layout(R, S);
   if (workspace_bytes < L.fixed + 512) return fail(TAPER_ERR_CAPACITY, "workspace too small");
   if (S == 0) { set_launches(0); return TAPER_OK; }
@@ -1214,6 +1223,7 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   AttnParams ap;
   ap.slot_page_off = kv->slot_page_off;
   ap.slot_pages = kv->slot_pages;
+  ap.seg_page_off = kv->seg_page_off;
   ap.req_page_off = kv->req_page_off;
   ap.req_pages = kv->req_pages;
   ap.hdr = reinterpret_cast<int32_t *>(w + L.hdr);

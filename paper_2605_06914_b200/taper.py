@@ -46,7 +46,7 @@ CTX_COUNTING = {"per_sequence": 0, "per_request": 1}
 class _Batch(ctypes.Structure):
     _fields_ = [("n_req", ctypes.c_int32), ("n_slot", ctypes.c_int32),
                 ("req_shared_len", _vp), ("req_slot_off", _vp), ("req_slack_ms", _vp),
-                ("slot_local_len", _vp)]
+                ("slot_local_len", _vp), ("slot_seg_off", _vp), ("seg_len", _vp)]
 
 
 class _Admission(ctypes.Structure):
@@ -58,7 +58,7 @@ class _KV(ctypes.Structure):
     _fields_ = [("k_pages", _vp), ("v_pages", _vp), ("num_pages", ctypes.c_int32),
                 ("page_size", ctypes.c_int32), ("h_local", ctypes.c_int32),
                 ("req_page_off", _vp), ("req_pages", _vp), ("slot_page_off", _vp),
-                ("slot_pages", _vp)]
+                ("slot_pages", _vp), ("seg_page_off", _vp)]
 
 
 def load_library() -> ctypes.CDLL:
@@ -143,6 +143,8 @@ class DeviceBatch:
     req_slot_off: torch.Tensor    # int32 [R+1]
     req_slack_ms: torch.Tensor    # float64 [R]
     slot_local_len: torch.Tensor  # int32 [S]
+    slot_seg_off: torch.Tensor | None = None  # int32 [S+1] local segments (reduce steps)
+    seg_len: torch.Tensor | None = None       # int32 [n_seg]
 
     @property
     def n_req(self):
@@ -155,12 +157,17 @@ class DeviceBatch:
     @classmethod
     def from_host(cls, b, device="cuda") -> "DeviceBatch":
         t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(device=device, dtype=dt)
+        seg_off = getattr(b, "slot_seg_off", None)
+        seg = None if seg_off is None else (t(seg_off, torch.int32),
+                                            t(b.seg_len if len(b.seg_len) else [0], torch.int32))
         return cls(t(b.req_shared_len, torch.int32), t(b.req_slot_off, torch.int32),
-                   t(b.req_slack_ms, torch.float64), t(b.slot_local_len, torch.int32))
+                   t(b.req_slack_ms, torch.float64), t(b.slot_local_len, torch.int32),
+                   *(seg or ()))
 
     def c(self) -> _Batch:
         return _Batch(self.n_req, self.n_slot, _ptr(self.req_shared_len), _ptr(self.req_slot_off),
-                      _ptr(self.req_slack_ms), _ptr(self.slot_local_len))
+                      _ptr(self.req_slack_ms), _ptr(self.slot_local_len), _ptr(self.slot_seg_off),
+                      _ptr(self.seg_len))
 
 
 @dataclass
@@ -193,11 +200,13 @@ class DeviceKV:
     req_pages: torch.Tensor
     slot_page_off: torch.Tensor
     slot_pages: torch.Tensor
+    seg_page_off: torch.Tensor | None = None  # int32 [n_seg] with DeviceBatch.slot_seg_off
 
     def c(self) -> _KV:
         n, h, ps, d = self.k_pages.shape
         return _KV(_ptr(self.k_pages), _ptr(self.v_pages), n, ps, h, _ptr(self.req_page_off),
-                   _ptr(self.req_pages), _ptr(self.slot_page_off), _ptr(self.slot_pages))
+                   _ptr(self.req_pages), _ptr(self.slot_page_off), _ptr(self.slot_pages),
+                   _ptr(self.seg_page_off))
 
 
 def page_tables_to_device(layout, device="cuda"):
@@ -211,16 +220,19 @@ TAPER_TILE_TOKENS = 64
 TAPER_LOCAL_ITEM_TILES = 16
 
 
-def max_chunk_slots(req_shared_len, req_slot_off, slot_local_len) -> int:
+def max_chunk_slots(req_shared_len, req_slot_off, slot_local_len, seg_len=None) -> int:
     """Eager-case partial-row count for taper_workspace_size: per request, its ready
-    branches x prefix chunks of 1024 tokens, plus one local item per <= 16 64-token tiles
-    of each branch's own segment (include/taper.h)."""
+    branches x prefix chunks of TAPER_CHUNK_TOKENS tokens, plus one local item per <= 16
+    64-token tiles of each branch's own segment (or of each local segment, if given;
+    include/taper.h)."""
     lsh = np.asarray(req_shared_len, np.int64)
     off = np.asarray(req_slot_off, np.int64)
     lloc = np.asarray(slot_local_len, np.int64)
     n = off[1:] - off[:-1]
     chunks = (lsh + TAPER_CHUNK_TOKENS - 1) // TAPER_CHUNK_TOKENS
     per_item = TAPER_TILE_TOKENS * TAPER_LOCAL_ITEM_TILES
+    if seg_len is not None:
+        lloc = np.asarray(seg_len, np.int64)
     local_items = (lloc + per_item - 1) // per_item
     return int((n * chunks).sum() + local_items.sum())
 

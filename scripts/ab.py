@@ -23,7 +23,8 @@ res = {n: [] for n, _ in variants}
 for rnd in range(3):
     for name, lib in variants:
         env = dict(os.environ, TAPER_LIB=lib)
-        out = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", os.environ.get("AB_SCRIPT", "steady.py"))],
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", os.environ.get("AB_SCRIPT", "steady.py")),
+                              *os.environ.get("AB_ARGS", "").split()],
                              env=env, capture_output=True, text=True)
         val = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-300:]
         res[name].append(val)

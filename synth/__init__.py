@@ -42,6 +42,8 @@ class Batch:
     req_slack_ms: np.ndarray     # float64 [R] d_r(t) - t
     slot_local_len: np.ndarray   # int32 [S]   Lloc_s
     req_serial: np.ndarray = field(default=None)  # bool [R] (info only)
+    slot_seg_off: np.ndarray = field(default=None)  # int32 [S+1] local segments, or None
+    seg_len: np.ndarray = field(default=None)       # int32 [n_seg]
 
     @property
     def n_req(self) -> int:
@@ -61,6 +63,7 @@ class Layout:
     req_pages: np.ndarray      # int32
     slot_page_off: np.ndarray  # int32 [S+1]
     slot_pages: np.ndarray     # int32
+    seg_page_off: np.ndarray = None  # int32 [n_seg]: first page of each local segment
 
 
 def _csr(counts) -> np.ndarray:
@@ -154,8 +157,21 @@ def make_layout(batch: Batch, page_size: int = PAGE, rng=None, spare_pages: int 
                 local_capacity: int | None = None) -> Layout:
     """Give every shared segment ceil(Lsh/page) pages and every slot's local segment
     ceil(max(Lloc, local_capacity)/page) pages, drawn as a random permutation of
-    the pool (so segments are not contiguous)."""
+    the pool (so segments are not contiguous).  A batch with local segments gets
+    ceil(seg_len/page) pages per segment instead (each segment starts on a page)."""
     rng = rng or np.random.default_rng(1)
+    if batch.slot_seg_off is not None:
+        need_sh = (batch.req_shared_len.astype(np.int64) + page_size - 1) // page_size
+        need_seg = (batch.seg_len.astype(np.int64) + page_size - 1) // page_size
+        total = int(need_sh.sum() + need_seg.sum()) + spare_pages
+        perm = rng.permutation(max(total, 1)).astype(np.int32)
+        seg_page_off = _csr(need_seg)
+        so = batch.slot_seg_off
+        per_slot = [int(need_seg[so[i]:so[i + 1]].sum()) for i in range(batch.n_slot)]
+        return Layout(page_size, max(total, 1), _csr(need_sh),
+                      np.ascontiguousarray(perm[: need_sh.sum()]), _csr(per_slot),
+                      np.ascontiguousarray(perm[need_sh.sum(): need_sh.sum() + need_seg.sum()]),
+                      np.ascontiguousarray(seg_page_off[:-1]))
     need_sh = (batch.req_shared_len.astype(np.int64) + page_size - 1) // page_size
     loc = batch.slot_local_len.astype(np.int64)
     if local_capacity is not None:
@@ -314,3 +330,43 @@ def utility_table(rng, R: int, K: int, kind: str = "concave") -> np.ndarray:
     elif kind != "concave":
         raise ValueError(kind)
     return np.concatenate([np.zeros((R, 1)), np.cumsum(inc, axis=1)], axis=1)
+
+
+def with_segments(batch: Batch, seg_lens_per_slot) -> Batch:
+    """Attach multi-segment local contexts: ``seg_lens_per_slot[s]`` lists the lengths of
+    slot s's local segments in order (their sum becomes Lloc_s)."""
+    counts = [len(x) for x in seg_lens_per_slot]
+    flat = [int(v) for x in seg_lens_per_slot for v in x]
+    batch.slot_seg_off = _csr(counts)
+    batch.seg_len = np.asarray(flat, np.int32)
+    batch.slot_local_len = np.asarray([sum(x) for x in seg_lens_per_slot], np.int32)
+    return batch
+
+
+def reduce_batch(seed: int = 0, n_serial=16, n_parallel=16, n_reduce=16, prefix=4096,
+                 slack_min_ms=1e3) -> Batch:
+    """Reduce-step mix (Sec. 3.1): serial requests,
+    parallel-phase requests (Table-4 fanout, one local segment of U{1..256} per branch) and
+    reduce-phase requests whose single slot sees P (+) H (shared, ``prefix`` tokens) then
+    every finished branch's h_i (+) y_i in canonical order (n ~ Table-4 fanout, lengths
+    U{32..512}) then the reduce tokens z so far (U{1..128}) -- each a segment in its own
+    pages, so the step reads the branches' KV where it lies."""
+    rng = np.random.default_rng(seed)
+    R = n_serial + n_parallel + n_reduce
+    kinds = rng.permutation(np.array([0] * n_serial + [1] * n_parallel + [2] * n_reduce))
+    fan, segs = [], []
+    for k in kinds:
+        if k == 0:
+            fan.append(1)
+            segs.append([])
+        elif k == 1:
+            n = int(sample_fanout(rng, 1)[0])
+            fan.append(n)
+            segs += [[int(rng.integers(1, 257))] for _ in range(n)]
+        else:
+            n = int(sample_fanout(rng, 1)[0])
+            fan.append(1)
+            segs.append([int(x) for x in rng.integers(32, 513, size=n)] + [int(rng.integers(1, 129))])
+    b = make_batch(np.full(R, prefix), fan, [sum(x) for x in segs], slack_min_ms, 20.0,
+                   serial=kinds != 1, rng=rng)
+    return with_segments(b, segs)

@@ -38,12 +38,16 @@ class Case:
         db = T.DeviceBatch.from_host(b, dev)
         adm = T.DeviceAdmission.empty(b.n_req, b.n_slot, dev)
         ws_bytes = T.taper_workspace_size(b.n_req, b.n_slot, h,
-                                          T.max_chunk_slots(b.req_shared_len, b.req_slot_off, b.slot_local_len))
+                                          T.max_chunk_slots(b.req_shared_len, b.req_slot_off,
+                                                            b.slot_local_len, b.seg_len))
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         T.taper_admit(db, model, policy, rho, adm, h, ws, cap)
         rpo, rp, spo, sp = T.page_tables_to_device(self.layout, dev)
+        spg = None
+        if self.layout.seg_page_off is not None:
+            spg = torch.as_tensor(np.concatenate([self.layout.seg_page_off, [0]]).astype(np.int32)).to(dev)
         kv = T.DeviceKV(self.k[:, g0:g1].contiguous().to(dev), self.v[:, g0:g1].contiguous().to(dev),
-                        rpo, rp, spo, sp)
+                        rpo, rp, spo, sp, spg)
         q = self.q[:, 8 * g0:8 * g1].contiguous().to(dev)
         out = torch.full_like(q, float("nan"))
         lse = torch.full((b.n_slot, 8 * h), float("nan"), device=dev) if with_lse else None
@@ -57,7 +61,7 @@ class Case:
         return oracle.attention(b.req_slot_off, b.req_shared_len, b.slot_local_len,
                                 lay.req_page_off, lay.req_pages, lay.slot_page_off,
                                 lay.slot_pages, self.k, self.v, self.q, slots, qheads,
-                                self.scale)
+                                self.scale, b.slot_seg_off, b.seg_len, lay.seg_page_off)
 
 
 def assert_close(gpu: np.ndarray, ref: np.ndarray, what=""):

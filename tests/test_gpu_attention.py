@@ -161,3 +161,43 @@ def test_garbage_past_sequence_end(page):
     adm_slots = np.flatnonzero(adm.slot_admitted.cpu().numpy()[:b.n_slot])
     assert torch.isfinite(out[adm_slots]).all()
     _check_all(case, adm, out, lse, what=f"nan tail page={page}")
+
+
+# ------------------------------------------------------------ multi-segment local context
+# Reduce steps (Sec. 3.1): the slot's local context is several segments (the
+# finished branches' h_i (+) y_i in canonical order, then z), each in its own pages.
+
+@pytest.mark.parametrize("variant", ["flat", "peaked"])
+@pytest.mark.parametrize("page", [16, 64])
+def test_reduce_segments_small(variant, page):
+    rng = np.random.default_rng(21)
+    b = synth.make_batch([300, 0, 70, 4100, 5], [1, 1, 3, 1, 2], [0] * 8, 1e3, 0.0, rng=rng)
+    segs = [[17, 64, 1, 130], [1, 63, 65], [5], [200], [77], [1500, 3, 40, 2200], [], [9, 9]]
+    b = synth.with_segments(b, segs)
+    case = Case(b, page=page, seed=6, variant=variant)
+    adm, out, lse = case.run_gpu(policy="eager")
+    _check_all(case, adm, out, lse, what=f"segments {variant} page={page}")
+
+
+def test_reduce_batch_sampled():
+    """Reduce-step mix at the C2 prefix size (4096): serial, parallel-phase and reduce-phase
+    requests (2-10 branch segments + z); every admitted slot x 4 sampled heads."""
+    b = synth.reduce_batch(seed=3)
+    case = Case(b, seed=3)
+    adm, out, lse = case.run_gpu(policy="eager")
+    heads = [0, 17, 42, 63]
+    _check_all(case, adm, out, lse, heads=heads, what="reduce mix")
+
+
+def test_segments_not_summing_to_local_length_flagged():
+    from paper_2605_06914_b200 import taper as T
+    b = synth.make_batch([64, 32], [1, 2], [0, 0, 0], 1e3, 0.0)
+    b = synth.with_segments(b, [[10, 20], [5], [7]])
+    b.seg_len = b.seg_len.copy()
+    b.seg_len[1] = 21  # slot 0: 10 + 21 != 30
+    db = T.DeviceBatch.from_host(b)
+    adm = T.DeviceAdmission.empty(b.n_req, b.n_slot)
+    ws = torch.empty(T.taper_workspace_size(2, 3, 8, 64), dtype=torch.uint8, device="cuda")
+    T.taper_admit(db, (1.0, 0.1, 0.01), "eager", 0.8, adm, 8, ws)
+    assert int(adm.status.item()) & T.TAPER_STATUS_BAD_LENGTH
+    assert int(adm.n_adm.item()) == 0

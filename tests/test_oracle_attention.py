@@ -178,3 +178,85 @@ def test_empty_context_is_an_error():
     b, lay, k, v, q = _case([0], [1], [0])
     with pytest.raises(ValueError):
         _run(b, lay, k, v, q, [0], [0])
+
+
+# ------------------------------------------------------------ multi-segment local context
+# Sec. 3.1 (L104-107): a reduce step attends to P (+) H (+) every branch's h_i (+) y_i in
+# canonical order (+) z; each branch's KV stays in its own pages (local segments).
+
+def _seg_case(page=16, seed=4):
+    b = synth.make_batch([40, 0, 23], [1, 1, 2], [0, 0, 0, 0], 10.0, 0.0)
+    b = synth.with_segments(b, [[5, 17, 1, 9], [33, 2], [], [16]])
+    lay = synth.make_layout(b, page, np.random.default_rng(seed), spare_pages=2)
+    k, v = synth.make_kv(lay.num_pages, 2, page, 32, seed)
+    q = synth.make_q(b.n_slot, 16, 32, seed)
+    return b, lay, k, v, q
+
+
+def _run_seg(b, lay, k, v, q, es, eh):
+    return oracle.attention(b.req_slot_off, b.req_shared_len, b.slot_local_len, lay.req_page_off,
+                            lay.req_pages, lay.slot_page_off, lay.slot_pages, k, v, q, es, eh,
+                            None, b.slot_seg_off, b.seg_len, lay.seg_page_off)
+
+
+def test_segments_match_torch_sdpa_fp64():
+    b, lay, k, v, q = _seg_case()
+    es, eh = _all_pairs(b, 16)
+    out, lse = _run_seg(b, lay, k, v, q, es, eh)
+    page = lay.page_size
+    for i, (s, hq) in enumerate(zip(es, eh)):
+        g = hq // 8
+        r = int(np.searchsorted(b.req_slot_off, s, side="right") - 1)
+        rows_k, rows_v = [], []
+        for t in range(int(b.req_shared_len[r])):
+            p = lay.req_pages[lay.req_page_off[r] + t // page]
+            rows_k.append(k[p, g, t % page]); rows_v.append(v[p, g, t % page])
+        for qs in range(b.slot_seg_off[s], b.slot_seg_off[s + 1]):  # segments in order
+            for t in range(int(b.seg_len[qs])):
+                p = lay.slot_pages[lay.seg_page_off[qs] + t // page]
+                rows_k.append(k[p, g, t % page]); rows_v.append(v[p, g, t % page])
+        K, V = torch.stack(rows_k).double(), torch.stack(rows_v).double()
+        qq = q[s, hq].double()
+        ref = torch.nn.functional.scaled_dot_product_attention(
+            qq[None, None, None], K[None, None], V[None, None])[0, 0, 0]
+        np.testing.assert_allclose(out[i], ref.numpy(), rtol=1e-12, atol=1e-13)
+        assert abs(lse[i] - torch.logsumexp(K @ qq / np.sqrt(32), 0).item()) < 1e-12
+
+
+def test_segments_equal_contiguous_copy():
+    """The same logical tokens in per-segment pages and copied into one contiguous local
+    segment give bit-identical outputs (the segment walk only locates tokens)."""
+    b, lay, k, v, q = _seg_case()
+    import copy
+    bc = copy.deepcopy(b)
+    bc.slot_seg_off = None
+    bc.seg_len = None
+    lay_c = synth.make_layout(bc, lay.page_size, np.random.default_rng(9), spare_pages=2)
+    kc = torch.zeros((lay_c.num_pages,) + tuple(k.shape[1:]), dtype=k.dtype)
+    vc = torch.zeros_like(kc)
+    ps = lay.page_size
+    for r in range(b.n_req):
+        for t in range(int(b.req_shared_len[r])):
+            src = lay.req_pages[lay.req_page_off[r] + t // ps]
+            dst = lay_c.req_pages[lay_c.req_page_off[r] + t // ps]
+            kc[dst, :, t % ps] = k[src, :, t % ps]; vc[dst, :, t % ps] = v[src, :, t % ps]
+    for s in range(b.n_slot):
+        u = 0
+        for qs in range(b.slot_seg_off[s], b.slot_seg_off[s + 1]):
+            for t in range(int(b.seg_len[qs])):
+                src = lay.slot_pages[lay.seg_page_off[qs] + t // ps]
+                dst = lay_c.slot_pages[lay_c.slot_page_off[s] + u // ps]
+                kc[dst, :, u % ps] = k[src, :, t % ps]; vc[dst, :, u % ps] = v[src, :, t % ps]
+                u += 1
+    es, eh = _all_pairs(b, 16)
+    o1, l1 = _run_seg(b, lay, k, v, q, es, eh)
+    o2, l2 = _run(bc, lay_c, kc, vc, q, es, eh)
+    assert (o1 == o2).all() and (l1 == l2).all()
+
+
+def test_segments_must_sum_to_local_length():
+    b, lay, k, v, q = _seg_case()
+    b.seg_len = b.seg_len.copy()
+    b.seg_len[0] += 1
+    with pytest.raises(ValueError):
+        _run_seg(b, lay, k, v, q, np.array([0]), np.array([0]))
