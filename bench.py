@@ -259,7 +259,7 @@ def run_ours(args):
     db = T.DeviceBatch.from_host(batch, dev)
     adm = T.DeviceAdmission.empty(R, S, dev)
     ws = torch.empty(T.taper_workspace_size(R, S, h, T.max_chunk_slots(batch.req_shared_len, batch.req_slot_off,
-                                                     batch.slot_local_len)),
+                                                     batch.slot_local_len, h_local=h)),
                      dtype=torch.uint8, device=dev)
     T.taper_admit(db, MODEL, "off", RHO, adm, h, ws)
     T0 = float(adm.diag[0].item())

@@ -63,9 +63,28 @@ extern "C" {
 #define TAPER_HEAD_DIM 128     /* Qwen3-32B head_dim                     */
 #define TAPER_GQA_GROUP 8      /* 64 Q heads / 8 KV heads (L359)                         */
 #ifndef TAPER_CHUNK_TOKENS
-#define TAPER_CHUNK_TOKENS 4096 /* shared-prefix split size: a fixed function of the
-                                   prefix length only (schedule invariance, Lemma 1)     */
+#define TAPER_CHUNK_TOKENS 4096 /* largest shared-prefix split (one work item's span)    */
 #endif
+/* Shared-prefix split of request r on a rank holding h_local KV heads: chunks of
+ *     clamp(roundup_64(max(512 * h_local, Lsh_r / 8)), 1024, TAPER_CHUNK_TOKENS)
+ * tokens -- 4096 for a 4k prefix at h_local = 8, 1024 at h_local <= 2, longer prefixes keep
+ * longer chunks (fewer partials) -- so a rank's work items stay plentiful when G > 1 GPUs
+ * split the heads (measured: DESIGN.md).  Chunk boundaries depend only on Lsh_r and
+ * h_local, never on which branches, siblings or other requests are admitted (schedule
+ * invariance, Lemma 1).                                                         */
+#if defined(__CUDACC__)
+#define TAPER_HD __host__ __device__
+#else
+#define TAPER_HD
+#endif
+static inline TAPER_HD int32_t taper_chunk_tokens(int32_t lsh, int32_t h_local) {
+  int32_t c = 512 * h_local;
+  if (lsh / 8 > c) c = lsh / 8;
+  c = (c + 63) / 64 * 64;
+  if (c < 1024) c = 1024;
+  if (c > TAPER_CHUNK_TOKENS) c = TAPER_CHUNK_TOKENS;
+  return c;
+}
 
 /* App. C.1 display eq. (L316): T(S) = a + b*n_tokens + c*L_context, in ms. [host]      */
 typedef struct {
@@ -162,7 +181,7 @@ typedef struct {
 
 /* Workspace bytes for a batch of at most n_req requests / n_slot slots on a rank with
  * h_local KV heads.  max_chunk_slots bounds the partial rows' count
- *     sum_r w_r * ceil(Lsh_r / TAPER_CHUNK_TOKENS)  +  sum_{s admitted} ceil(Lloc_s / 1024)
+ *     sum_r w_r * ceil(Lsh_r / taper_chunk_tokens(Lsh_r, h_local))  +  sum_{s admitted} ceil(Lloc_s / 1024)
  * (prefix chunks per admitted branch, plus one per local item of <= 16 64-token tiles;
  * with local segments the second sum runs over segments: sum ceil(seg_len / 1024));
  * the Eager value of that sum over all ready slots is always enough.  An undersized

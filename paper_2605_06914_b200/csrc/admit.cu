@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
   }
 
   // ---- work list (A5): per-request widths, item counts and CSR offsets.
-  // Shared items: (TAPER_CHUNK_TOKENS prefix chunk, group of <= 8 admitted branches).  Local items:
+  // Shared items: (taper_chunk_tokens(Lsh_r, h_local)-token prefix chunk, group of <= 8 admitted branches).  Local items:
   // <= kLocalItemTiles 64-token tiles of ONE admitted branch's local KV.  Partials (8 rows
   // per KV head each): shared (chunk c, branch j) at c * w + j, then one per local item.
   int w_loc[kPerThread], nc_loc[kPerThread], nl_loc[kPerThread], cs_loc[kPerThread];
@@ -455,7 +455,10 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
             w += 1;
             nl += local_items(p, s);
           }
-        if (w > 0 && p.Lsh[r] > 0) nc = (p.Lsh[r] + kChunk - 1) / kChunk;
+        if (w > 0 && p.Lsh[r] > 0) {
+          const int ck = taper_chunk_tokens(p.Lsh[r], p.h_local);
+          nc = (p.Lsh[r] + ck - 1) / ck;
+        }
       }
       p.req_width[r] = w;
     }
@@ -510,6 +513,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     const int nc = nsh / groups;
     const int cs_r = p.req_part_off[r];
     const int it0 = p.req_chunk_off[r] + p.req_loc_off[r];  // request-major item numbering
+    const int ck = taper_chunk_tokens(p.Lsh[r], p.h_local);  // include/taper.h
     for (int c = 0; c < nc; ++c)
       for (int g = 0; g < groups; ++g) {
         ItemDesc d;
@@ -517,7 +521,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
         d.w = min(kMaxItemBranches, w - g * kMaxItemBranches);
         d.adm_off = adm_off + g * kMaxItemBranches;
         d.cs0 = cs_r + c * w + g * kMaxItemBranches;
-        d.tb = c * kChunk; d.te = min(d.tb + kChunk, p.Lsh[r]);
+        d.tb = c * ck; d.te = min(d.tb + ck, p.Lsh[r]);
         d.nt = (d.te - d.tb + kTileTokens - 1) / kTileTokens;
         d.flags = 0;
         p.items[it0 + c * groups + g] = d;

@@ -220,7 +220,16 @@ TAPER_TILE_TOKENS = 64
 TAPER_LOCAL_ITEM_TILES = 16
 
 
-def max_chunk_slots(req_shared_len, req_slot_off, slot_local_len, seg_len=None) -> int:
+def chunk_tokens(lsh, h_local: int):
+    """taper_chunk_tokens(Lsh, h_local) of include/taper.h (vectorised): the shared-prefix
+    split clamp(roundup_64(max(512 h, Lsh / 8)), 1024, 4096) -- sizing only."""
+    c = np.maximum(512 * h_local, np.asarray(lsh, np.int64) // 8)
+    c = (c + 63) // 64 * 64
+    return np.clip(c, 1024, TAPER_CHUNK_TOKENS)
+
+
+def max_chunk_slots(req_shared_len, req_slot_off, slot_local_len, seg_len=None,
+                    h_local: int = 1) -> int:
     """Eager-case partial-row count for taper_workspace_size: per request, its ready
     branches x prefix chunks of TAPER_CHUNK_TOKENS tokens, plus one local item per <= 16
     64-token tiles of each branch's own segment (or of each local segment, if given;
@@ -229,7 +238,8 @@ def max_chunk_slots(req_shared_len, req_slot_off, slot_local_len, seg_len=None) 
     off = np.asarray(req_slot_off, np.int64)
     lloc = np.asarray(slot_local_len, np.int64)
     n = off[1:] - off[:-1]
-    chunks = (lsh + TAPER_CHUNK_TOKENS - 1) // TAPER_CHUNK_TOKENS
+    ck = chunk_tokens(lsh, h_local)  # default h_local = 1: the finest split (always enough)
+    chunks = (lsh + ck - 1) // ck
     per_item = TAPER_TILE_TOKENS * TAPER_LOCAL_ITEM_TILES
     if seg_len is not None:
         lloc = np.asarray(seg_len, np.int64)

@@ -17,22 +17,25 @@ def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
     n_pools = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     n_calls = int(sys.argv[3]) if len(sys.argv) > 3 else 32
+    h = int(sys.argv[4]) if len(sys.argv) > 4 else 8  # KV heads of the rank (8 / G)
     b = synth.config_batch(cfg, seed=0)
     lay = synth.make_layout(b, 64, np.random.default_rng(1), 1)
     db = T.DeviceBatch.from_host(b)
     adm = T.DeviceAdmission.empty(b.n_req, b.n_slot)
-    ws = torch.empty(T.taper_workspace_size(b.n_req, b.n_slot, 8, T.max_chunk_slots(
+    # 2x the h = 1 bound: room for experimental finer splits (TAPER_CHUNK_MIN variants)
+    ws = torch.empty(T.taper_workspace_size(b.n_req, b.n_slot, h, 2 * T.max_chunk_slots(
         b.req_shared_len, b.req_slot_off, b.slot_local_len)), dtype=torch.uint8, device="cuda")
-    T.taper_admit(db, (12.0, 0.03, 2e-5), "eager", 0.8, adm, 8, ws)
+    T.taper_admit(db, (12.0, 0.03, 2e-5), "eager", 0.8, adm, h, ws)
+    assert int(adm.status.item()) == 0, T.taper_status_string(int(adm.status.item()))
     g = torch.Generator(device="cuda").manual_seed(0)
-    shape = (lay.num_pages, 8, 64, 128)
+    shape = (lay.num_pages, h, 64, 128)
     rpo, rp, spo, sp = T.page_tables_to_device(lay)
     pools = []
     for _ in range(n_pools):
         k = torch.randn(shape, generator=g, device="cuda", dtype=torch.bfloat16)
         v = torch.randn(shape, generator=g, device="cuda", dtype=torch.bfloat16)
         pools.append(T.DeviceKV(k, v, rpo, rp, spo, sp))
-    q = torch.randn((b.n_slot, 64, 128), generator=g, device="cuda", dtype=torch.bfloat16)
+    q = torch.randn((b.n_slot, 8 * h, 128), generator=g, device="cuda", dtype=torch.bfloat16)
     out = torch.empty_like(q)
     sc = 1 / math.sqrt(128)
     for i in range(n_pools):

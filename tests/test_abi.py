@@ -42,4 +42,10 @@ def test_host_validation_without_gpu():
     assert "precision" in T.taper_status_string(4)
     # 4096-token prefix chunks x ready branches (3 x 1 + 1 x 1 + 2 x 0) + one local item per
     # branch with local tokens (65, 1, 2, 3 -> 4 items of <= 16 x 64 tokens)
-    assert T.max_chunk_slots([4097, 1, 0], [0, 3, 4, 6], [0, 65, 1, 0, 2, 3]) == 6 + 1 + 0 + 4
+    assert T.max_chunk_slots([4097, 1, 0], [0, 3, 4, 6], [0, 65, 1, 0, 2, 3], h_local=8) == 6 + 1 + 0 + 4
+    # taper_chunk_tokens(Lsh, h) (include/taper.h): 4k prefix -> 1024 at h <= 2, 2048 at
+    # h = 4, 4096 at h = 8; a 24k prefix keeps 3072-token chunks at any h < 8
+    assert [int(T.chunk_tokens(4096, h)) for h in (1, 2, 4, 8)] == [1024, 1024, 2048, 4096]
+    assert [int(T.chunk_tokens(24576, h)) for h in (1, 4, 8)] == [3072, 3072, 4096]
+    assert int(T.chunk_tokens(100, 8)) == 4096 and int(T.chunk_tokens(100, 1)) == 1024
+    assert T.max_chunk_slots([4097, 1, 0], [0, 3, 4, 6], [0, 65, 1, 0, 2, 3]) == 15 + 1 + 0 + 4
