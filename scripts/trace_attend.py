@@ -18,20 +18,21 @@ EV = ["tma_issue", "mma_full", "qk_commit", "pv_pfull", "pv_ofree", "pv_commit",
 def main():
     global _fn
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    h = int(sys.argv[2]) if len(sys.argv) > 2 else 8  # KV heads of the rank (8 / G)
     b = synth.config_batch(cfg, seed=0)
     lay = synth.make_layout(b, 64, np.random.default_rng(1), 1)
     db = T.DeviceBatch.from_host(b)
     adm = T.DeviceAdmission.empty(b.n_req, b.n_slot)
-    ws = torch.empty(T.taper_workspace_size(b.n_req, b.n_slot, 8, T.max_chunk_slots(
+    ws = torch.empty(T.taper_workspace_size(b.n_req, b.n_slot, h, T.max_chunk_slots(
         b.req_shared_len, b.req_slot_off, b.slot_local_len)), dtype=torch.uint8, device="cuda")
-    T.taper_admit(db, (12.0, 0.03, 2e-5), "eager", 0.8, adm, 8, ws)
+    T.taper_admit(db, (12.0, 0.03, 2e-5), "eager", 0.8, adm, h, ws)
     g = torch.Generator(device="cuda").manual_seed(0)
-    shape = (lay.num_pages, 8, 64, 128)
+    shape = (lay.num_pages, h, 64, 128)
     k = torch.randn(shape, generator=g, device="cuda", dtype=torch.bfloat16)
     v = torch.randn(shape, generator=g, device="cuda", dtype=torch.bfloat16)
     rpo, rp, spo, sp = T.page_tables_to_device(lay)
     kv = T.DeviceKV(k, v, rpo, rp, spo, sp)
-    q = torch.randn((b.n_slot, 64, 128), generator=g, device="cuda", dtype=torch.bfloat16)
+    q = torch.randn((b.n_slot, 8 * h, 128), generator=g, device="cuda", dtype=torch.bfloat16)
     out = torch.empty_like(q)
     for _ in range(3):
         T.taper_decode_attention(db, adm, kv, q, out, None, 1 / math.sqrt(128), ws)
