@@ -89,8 +89,10 @@ constexpr uint32_t kColS = 0;     // S^T 0 [0, 64), S^T 1 [64, 128): 64 tokens x
 constexpr uint32_t kColO = 128;   // O^T 0 [128, 256), O^T 1 [256, 384): 128 d x 2N rows
 
 struct AttnParams {
+  // slot_page_off: per slot (local tiles with segment -1) or, when the batch has local
+  // segments, taper_kv.seg_page_off per segment.  (One pointer for both: an extra kernel
+  // parameter measurably slowed the kernel, 200 -> 212 us per C2 layer.)
   const int32_t *slot_page_off, *slot_pages, *req_page_off, *req_pages;
-  const int32_t *seg_page_off;  // local segments' first page in slot_pages (NULL: unused)
   int32_t *hdr;        // hdr[8]: work counter, hdr[9]: CTAs exited
   const int32_t *adm_by_req;
   int32_t *done;       // [r * 8 + g]: items of (request, KV head) whose partials are written
@@ -146,7 +148,7 @@ __device__ __forceinline__ TileInfo tile_info(const AttnParams &p, const Item &x
     ti.valid = min(kTile, x.te - ti.tok0);
   } else {
     const int4 lt = __ldg(p.ltiles + x.tb + t);  // {slot, tok0, valid, segment or -1}
-    ti.pages = p.slot_pages + (lt.w >= 0 ? __ldg(p.seg_page_off + lt.w) : __ldg(p.slot_page_off + lt.x));
+    ti.pages = p.slot_pages + __ldg(p.slot_page_off + (lt.w >= 0 ? lt.w : lt.x));
     ti.tok0 = lt.y;
     ti.valid = lt.z;
   }
@@ -1221,9 +1223,8 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   }
   WsTables tabs = ws_tables(workspace_bytes, R, S, h);
   AttnParams ap;
-  ap.slot_page_off = kv->slot_page_off;
+  ap.slot_page_off = batch->slot_seg_off ? kv->seg_page_off : kv->slot_page_off;
   ap.slot_pages = kv->slot_pages;
-  ap.seg_page_off = kv->seg_page_off;
   ap.req_page_off = kv->req_page_off;
   ap.req_pages = kv->req_pages;
   ap.hdr = reinterpret_cast<int32_t *>(w + L.hdr);
