@@ -1,0 +1,65 @@
+"""NEXT-2 closed-loop harness (scripts/closed_loop.py), host logic on CPU: the literal
+Alg. 1 oracle admits, and a linear step-time model (App. C.1, cascade-aware context)
+stands in for the B200 step.  Checks the metric definitions (App. D) and the
+directional behaviour the paper reports: Eager buys throughput and loses attainment under
+load (the throughput trap, Sec. 2.2), TAPER keeps the SLO while admitting more than Off."""
+import importlib.util
+import os
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+_spec = importlib.util.spec_from_file_location("closed_loop", os.path.join(ROOT, "scripts", "closed_loop.py"))
+CL = importlib.util.module_from_spec(_spec)
+sys.modules["closed_loop"] = CL  # dataclasses resolve their module by name
+_spec.loader.exec_module(CL)
+
+# a B200-like predictor with the synthetic non-attention part (scripts/closed_loop.py)
+MODEL = (0.707 + CL.REST[0], 0.0107 + CL.REST[1], 4.07e-5)
+
+
+def _drivers():
+    def admit_fn(b, policy, rho):
+        kind, cap = CL.POLICY_ARGS[policy]
+        o = oracle.admit(b.req_shared_len, b.req_slot_off, b.req_slack_ms, b.slot_local_len,
+                         MODEL, kind, cap, rho, ctx="per_request")
+        assert (o.req_width >= 1).all()  # every active request advances (L128)
+        return o.slot_admitted.astype(bool)
+
+    def step_fn(b, adm):
+        off = b.req_slot_off
+        n = int(adm.sum())
+        L = 0
+        for r in range(b.n_req):
+            a = adm[off[r]:off[r + 1]]
+            if a.any():
+                L += int(b.req_shared_len[r]) + int(b.slot_local_len[off[r]:off[r + 1]][a].sum())
+        return MODEL[0] + MODEL[1] * n + MODEL[2] * L
+
+    return admit_fn, step_fn
+
+
+@pytest.fixture(scope="module")
+def results():
+    admit_fn, step_fn = _drivers()
+    return {p: CL.run(p, admit_fn, step_fn, 900, seed=1) for p in ("off", "eager", "taper")}
+
+
+def test_metric_definitions(results):
+    for r in results.values():
+        assert 0.0 <= r["attainment"] <= 1.0
+        assert r["goodput_tok_s"] <= r["throughput_tok_s"] + 1e-9
+        assert r["finished"] > 50
+
+
+def test_throughput_trap_directional(results):
+    off, eager, taper = results["off"], results["eager"], results["taper"]
+    assert off["admission_rate"] == 0.0 and eager["admission_rate"] == 1.0
+    assert 0.0 < taper["admission_rate"] < 1.0
+    assert eager["attainment"] < taper["attainment"]
+    assert taper["attainment"] >= 0.9
+    assert taper["goodput_tok_s"] > eager["goodput_tok_s"]
