@@ -51,6 +51,10 @@ static_assert(kItemTiles <= 64, "scheduler lanes resolve at most two tiles each"
 #ifndef TAPER_VSTAGES
 #define TAPER_VSTAGES 5
 #endif
+#ifndef TAPER_EARLY_CLAIM
+#define TAPER_EARLY_CLAIM 1
+#endif
+constexpr bool kEarlyClaim = TAPER_EARLY_CLAIM;
 constexpr int kKStages = TAPER_KSTAGES;
 constexpr int kVStages = TAPER_VSTAGES;
 constexpr int kStageBytes = 2 * 8192;
@@ -635,7 +639,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   // PDL: the prologue above overlapped the previous kernel; the merge kernel may launch now
   // (it waits for per-request completion counters); wait for the previous kernel's memory.
   pdl_launch_dependents();
-  pdl_wait();
+  // The scheduler warp claims and resolves its first item before waiting (see below).
+  if (!(kEarlyClaim && warp == 11)) pdl_wait();
 
   if (warp == 11) {
     // ======================= item scheduler ==================================================
@@ -651,7 +656,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     for (uint32_t k = 0;; ++k) {
       if (k >= 1) mbar_wait(sched_go, (k - 1) & 1);  // K producer started item k-1
       int it = 0;
-      if (lane == 0) it = atomicAdd(work_counter, 1);
+      // first item: claim index blockIdx.x (static), later ones from the counter
+      if (lane == 0)
+        it = (kEarlyClaim && k == 0) ? int(blockIdx.x)
+                                     : (kEarlyClaim ? int(gridDim.x) : 0) + atomicAdd(work_counter, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
       if (it >= n_items) it = -1;
       const uint32_t slot = k % kItemRing;
@@ -686,6 +694,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(it_full + slot);  // release: the record is visible
       if (it < 0) break;
+      // Early claim: the first record (descriptor, tiles, pages -- tables written by
+      // taper_admit or the caller before the previous kernel started) was resolved while the
+      // previous kernel finished; q may come from the kernel just before, so wait here.
+      if (kEarlyClaim && k == 0) pdl_wait();
       // Q^T of the item's w branches: box {64 d, 8 rows, 2 d-halves} of q viewed as
       // (d-lo, GQA row, d-half, slot * h + g) -> [d-half][8 rows][128 B] per branch
       const uint32_t qb = k & 1;

@@ -137,8 +137,44 @@ def advance(active, b, slot_admitted, now):
     return toks
 
 
-def run(policy, admit_fn, step_fn, n_steps, seed=0, rho=0.8):
+class RollingFit:
+    """App. C.2 (L337): the predictor is refreshed by OLS on a rolling window of the most
+    recent 200 observed step latencies (here every `every` steps instead of 10 minutes)."""
+
+    def __init__(self, model, window=200, every=50):
+        self.model, self.window, self.every = tuple(model), window, every
+        self.obs = []
+        self.count = 0
+
+    def observe(self, n, L, t):
+        self.obs.append((n, L, t))
+        self.obs = self.obs[-self.window:]
+        self.count += 1
+        if len(self.obs) >= 50 and self.count % self.every == 0:
+            X = np.array([[1.0, o[0], o[1]] for o in self.obs])
+            y = np.array([o[2] for o in self.obs])
+            coef, *_ = np.linalg.lstsq(X, y, rcond=None)
+            if coef[1] > 0 and coef[2] > 0 and coef[0] >= 0:  # keep T monotone (L341)
+                self.model = tuple(float(c) for c in coef)
+
+
+def context_per_request(b, adm):
+    """Cascade-aware L_context of the admitted set (reading R-ctx): prefix once per request."""
+    off = b.req_slot_off
+    L = 0
+    for r in range(b.n_req):
+        a = adm[off[r]:off[r + 1]]
+        if a.any():
+            L += int(b.req_shared_len[r]) + int(b.slot_local_len[off[r]:off[r + 1]][a].sum())
+    return L
+
+
+def run(policy, admit_fn, step_fn, n_steps, seed=0, rho=0.8, model=None, refit=True):
+    """admit_fn(batch, policy, rho, model) -> (slot mask, predicted T(S) ms);
+    step_fn(batch, mask) -> realised step ms."""
     rng = np.random.default_rng(seed)
+    fit = RollingFit(model) if model is not None else None
+    pred_err = []
     now, rid = 0.0, 0
     queue, active, finished = [], [], []
     tokens = 0
@@ -159,8 +195,11 @@ def run(policy, admit_fn, step_fn, n_steps, seed=0, rho=0.8):
             now += 1.0
             continue
         b = batch_of(active, now)
-        adm = admit_fn(b, policy, rho)
+        adm, t_pred = admit_fn(b, policy, rho, fit.model if fit else None)
         t = step_fn(b, adm)
+        pred_err.append((t - t_pred) / t)
+        if fit is not None and refit:
+            fit.observe(int(adm.sum()), context_per_request(b, adm), t)
         now += t
         step_ms.append(t)
         opp_ready += b.n_slot - b.n_req
@@ -184,6 +223,9 @@ def run(policy, admit_fn, step_fn, n_steps, seed=0, rho=0.8):
         "finished": len(finished),
         "mean_step_ms": float(np.mean(step_ms)), "p99_step_ms": float(np.percentile(step_ms, 99)),
         "admission_rate": opp_granted / max(1, opp_ready),
+        "predictor_rel_err_median": float(np.median(pred_err)),
+        "predictor_rel_err_p95_abs": float(np.percentile(np.abs(pred_err), 95)),
+        "final_model": fit.model if fit else None,
     }
 
 
@@ -208,13 +250,14 @@ def gpu_drivers(timed_layers):
     out = torch.empty_like(q)
     state = {}
 
-    def admit_fn(b, policy, rho):
+    def admit_fn(b, policy, rho, mdl):
         kind, cap = POLICY_ARGS[policy]
         db = T.DeviceBatch.from_host(b)
         adm = T.DeviceAdmission.empty(b.n_req, b.n_slot)
-        T.taper_admit(db, model, kind, rho, adm, 8, ws, cap, ctx="per_request")
+        T.taper_admit(db, mdl, kind, rho, adm, 8, ws, cap, ctx="per_request")
         state["db"], state["adm"] = db, adm
-        return adm.slot_admitted.cpu().numpy()[:b.n_slot].astype(bool)
+        return (adm.slot_admitted.cpu().numpy()[:b.n_slot].astype(bool),
+                float(adm.diag[2].item()))
 
     def step_fn(b, adm_mask):
         lay = synth.make_layout(b, 64, np.random.default_rng(len(b.slot_local_len)))
@@ -247,8 +290,11 @@ def main():
     runs = [(p, 0.8) for p in args.policies.split(",")]
     runs += [("taper", float(x)) for x in args.rhos.split(",") if x]
     res = []
+    runs += [("taper-norefit", 0.8)]
     for p, rho in runs:
-        r = run(p, admit_fn, step_fn, args.steps, rho=rho)
+        r = run(p.split("-")[0], admit_fn, step_fn, args.steps, rho=rho, model=model,
+                refit=not p.endswith("norefit"))
+        r["variant"] = p
         res.append(r)
         print(json.dumps(r), flush=True)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)

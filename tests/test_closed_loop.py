@@ -23,22 +23,15 @@ MODEL = (0.707 + CL.REST[0], 0.0107 + CL.REST[1], 4.07e-5)
 
 
 def _drivers():
-    def admit_fn(b, policy, rho):
+    def admit_fn(b, policy, rho, model):
         kind, cap = CL.POLICY_ARGS[policy]
         o = oracle.admit(b.req_shared_len, b.req_slot_off, b.req_slack_ms, b.slot_local_len,
-                         MODEL, kind, cap, rho, ctx="per_request")
+                         model, kind, cap, rho, ctx="per_request")
         assert (o.req_width >= 1).all()  # every active request advances (L128)
-        return o.slot_admitted.astype(bool)
+        return o.slot_admitted.astype(bool), o.T_S
 
     def step_fn(b, adm):
-        off = b.req_slot_off
-        n = int(adm.sum())
-        L = 0
-        for r in range(b.n_req):
-            a = adm[off[r]:off[r + 1]]
-            if a.any():
-                L += int(b.req_shared_len[r]) + int(b.slot_local_len[off[r]:off[r + 1]][a].sum())
-        return MODEL[0] + MODEL[1] * n + MODEL[2] * L
+        return MODEL[0] + MODEL[1] * int(adm.sum()) + MODEL[2] * CL.context_per_request(b, adm)
 
     return admit_fn, step_fn
 
@@ -46,7 +39,7 @@ def _drivers():
 @pytest.fixture(scope="module")
 def results():
     admit_fn, step_fn = _drivers()
-    return {p: CL.run(p, admit_fn, step_fn, 900, seed=1) for p in ("off", "eager", "taper")}
+    return {p: CL.run(p, admit_fn, step_fn, 900, seed=1, model=MODEL) for p in ("off", "eager", "taper")}
 
 
 def test_metric_definitions(results):
@@ -63,3 +56,12 @@ def test_throughput_trap_directional(results):
     assert eager["attainment"] < taper["attainment"]
     assert taper["attainment"] >= 0.9
     assert taper["goodput_tok_s"] > eager["goodput_tok_s"]
+
+
+def test_rolling_refit_recovers_the_step_model():
+    """App. C.2 (L337): OLS on the last 200 observed steps recovers the true (a, b, c)
+    from a biased starting model (exact linear clock, so the fit is exact)."""
+    admit_fn, step_fn = _drivers()
+    r = CL.run("taper", admit_fn, step_fn, 400, seed=2, model=(5.0, 0.05, 1e-5))
+    np.testing.assert_allclose(r["final_model"], MODEL, rtol=1e-6)
+    assert abs(r["predictor_rel_err_median"]) < 1e-6
