@@ -169,7 +169,7 @@ def context_per_request(b, adm):
     return L
 
 
-def run(policy, admit_fn, step_fn, n_steps, seed=0, rho=0.8, model=None, refit=True):
+def run(policy, admit_fn, step_fn, n_steps, seed=0, rho=0.8, model=None, refit=False):
     """admit_fn(batch, policy, rho, model) -> (slot mask, predicted T(S) ms);
     step_fn(batch, mask) -> realised step ms."""
     rng = np.random.default_rng(seed)
@@ -290,10 +290,10 @@ def main():
     runs = [(p, 0.8) for p in args.policies.split(",")]
     runs += [("taper", float(x)) for x in args.rhos.split(",") if x]
     res = []
-    runs += [("taper-norefit", 0.8)]
+    runs += [("taper-refit", 0.8)]  # App. C.2 rolling refresh (unstable here: see DESIGN)
     for p, rho in runs:
         r = run(p.split("-")[0], admit_fn, step_fn, args.steps, rho=rho, model=model,
-                refit=not p.endswith("norefit"))
+                refit=p.endswith("-refit"))
         r["variant"] = p
         res.append(r)
         print(json.dumps(r), flush=True)

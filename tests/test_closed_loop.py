@@ -62,6 +62,6 @@ def test_rolling_refit_recovers_the_step_model():
     """App. C.2 (L337): OLS on the last 200 observed steps recovers the true (a, b, c)
     from a biased starting model (exact linear clock, so the fit is exact)."""
     admit_fn, step_fn = _drivers()
-    r = CL.run("taper", admit_fn, step_fn, 400, seed=2, model=(5.0, 0.05, 1e-5))
+    r = CL.run("taper", admit_fn, step_fn, 400, seed=2, model=(5.0, 0.05, 1e-5), refit=True)
     np.testing.assert_allclose(r["final_model"], MODEL, rtol=1e-6)
     assert abs(r["predictor_rel_err_median"]) < 1e-6
