@@ -43,6 +43,9 @@ WORKLOADS = {
     "c5": "scaling sweep: 256 requests (128 serial + 128 parallel, Table-4 fanouts), prefixes "
           "log-U[1k,32k], branch-local U{1..256}, 64 layers",
     "c1": "tiny: 2 requests (1 serial, 1 with 4 branches), prefix 512, branch-local 32",
+    "reduce": "reduce-step mix (NEXT-4): 48 requests (16 serial, 16 parallel with Table-4 "
+              "fanouts, 16 reduce-phase attending to P+H plus 2-10 finished branches of "
+              "U{32..512} tokens and z, each in its own pages), prefix 4096, 64 layers",
 }
 
 
@@ -162,7 +165,8 @@ def cpu_baseline(batch, layout, adm_mask, seconds, seed, layers):
         t1 = time.perf_counter()
         oracle.attention(batch.req_slot_off, batch.req_shared_len, batch.slot_local_len,
                          layout.req_page_off, layout.req_pages, layout.slot_page_off,
-                         layout.slot_pages, k, v, q, np.full(64, s), np.arange(64))
+                         layout.slot_pages, k, v, q, np.full(64, s), np.arange(64), None,
+                         batch.slot_seg_off, batch.seg_len, layout.seg_page_off)
         t_att += time.perf_counter() - t1
         done += 1
         r = int(np.searchsorted(batch.req_slot_off, s, side="right") - 1)
@@ -184,6 +188,8 @@ def cpu_baseline(batch, layout, adm_mask, seconds, seed, layers):
 
 
 def build_batch(args):
+    if args.config == "reduce":
+        return synth.reduce_batch(seed=args.seed, slack_min_ms=1e6)
     return synth.config_batch(args.config, seed=args.seed, slack_min_ms=1e6)
 
 
@@ -259,7 +265,7 @@ def run_ours(args):
     db = T.DeviceBatch.from_host(batch, dev)
     adm = T.DeviceAdmission.empty(R, S, dev)
     ws = torch.empty(T.taper_workspace_size(R, S, h, T.max_chunk_slots(batch.req_shared_len, batch.req_slot_off,
-                                                     batch.slot_local_len, h_local=h)),
+                                                     batch.slot_local_len, batch.seg_len, h_local=h)),
                      dtype=torch.uint8, device=dev)
     T.taper_admit(db, MODEL, "off", RHO, adm, h, ws)
     T0 = float(adm.diag[0].item())
@@ -270,6 +276,8 @@ def run_ours(args):
 
     layout = synth.make_layout(batch, synth.PAGE, np.random.default_rng(args.seed + 1), 1)
     rpo, rp, spo, sp = T.page_tables_to_device(layout, dev)
+    spg = None if layout.seg_page_off is None else torch.as_tensor(  # reduce steps (NEXT-4)
+        np.concatenate([layout.seg_page_off, [0]]).astype(np.int32)).to(dev)
     layer_bytes = 2 * layout.num_pages * h * layout.page_size * 128 * 2
     n_distinct = max(1, min(L, int(KV_BUDGET_BYTES // layer_bytes)))
     gen = torch.Generator(device=dev)
@@ -279,7 +287,7 @@ def run_ours(args):
         shape = (layout.num_pages, h, layout.page_size, 128)
         k = torch.randn(shape, generator=gen, device=dev, dtype=torch.bfloat16)
         v = torch.randn(shape, generator=gen, device=dev, dtype=torch.bfloat16)
-        pools.append(T.DeviceKV(k, v, rpo, rp, spo, sp))
+        pools.append(T.DeviceKV(k, v, rpo, rp, spo, sp, spg))
     kvs = [pools[i % n_distinct] for i in range(L)]
     gen.manual_seed(99 + rank)
     qs = [torch.randn((S, 8 * h, 128), generator=gen, device=dev, dtype=torch.bfloat16)

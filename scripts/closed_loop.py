@@ -264,15 +264,18 @@ def gpu_drivers(timed_layers):
         assert lay.num_pages <= pool_pages, lay.num_pages
         rpo, rp, spo, sp = T.page_tables_to_device(lay)
         kv = T.DeviceKV(k, v, rpo, rp, spo, sp)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         sc = 1 / math.sqrt(128)
         T.taper_decode_attention(state["db"], state["adm"], kv, q, out, None, sc, ws)  # warm
-        e0.record()
-        for _ in range(timed_layers):
-            T.taper_decode_attention(state["db"], state["adm"], kv, q, out, None, sc, ws)
-        e1.record()
+        per = max(1, timed_layers // 3)
+        ev[0].record()
+        for i in range(3):  # three blocks of layers; the median block resists timing outliers
+            for _ in range(per):
+                T.taper_decode_attention(state["db"], state["adm"], kv, q, out, None, sc, ws)
+            ev[i + 1].record()
         torch.cuda.synchronize()
-        attn = e0.elapsed_time(e1) * 64 / timed_layers
+        blocks = [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
+        attn = float(np.median(blocks)) * 64 / per
         return attn + REST[0] + REST[1] * int(adm_mask.sum())
 
     return admit_fn, step_fn, model
@@ -283,7 +286,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1500)
     ap.add_argument("--policies", default="off,cap2,cap5,eager,taper")
     ap.add_argument("--rhos", default="0.5,1.0", help="extra TAPER rho sweep (Table 1)")
-    ap.add_argument("--timed-layers", type=int, default=16)
+    ap.add_argument("--timed-layers", type=int, default=24)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "closed_loop.json"))
     args = ap.parse_args()
     admit_fn, step_fn, model = gpu_drivers(args.timed_layers)

@@ -206,3 +206,21 @@ def test_segments_not_summing_to_local_length_flagged():
     T.taper_admit(db, (1.0, 0.1, 0.01), "eager", 0.8, adm, 8, ws)
     assert int(adm.status.item()) & T.TAPER_STATUS_BAD_LENGTH
     assert int(adm.n_adm.item()) == 0
+
+
+def test_max_slots_capacity():
+    """TAPER_MAX_SLOTS: 1024 requests x 4 branches = 4096 slots with short ragged contexts
+    (thousands of work items); sampled slots x heads against the oracle, every admitted
+    slot written."""
+    rng = np.random.default_rng(31)
+    R = 1024
+    b = synth.make_batch(rng.integers(0, 300, R), np.full(R, 4), rng.integers(1, 90, 4 * R),
+                         1e3, 0.0, rng=rng)
+    case = Case(b, seed=8)
+    adm, out, lse = case.run_gpu(policy="eager")
+    assert int(adm.n_adm.item()) == 4096
+    assert torch.isfinite(out.float()).all()
+    slots = np.sort(rng.choice(4096, 96, replace=False))
+    es, eh = np.repeat(slots, 2), np.tile([5, 60], len(slots))
+    ref, ref_lse = case.run_oracle(es, eh)
+    assert_close(out[es, eh].float().numpy(), ref, "max slots")
