@@ -19,6 +19,10 @@ namespace taper {
 
 constexpr int kAdmitThreads = 1024;
 constexpr int kPerThread = kMaxSlots / kAdmitThreads;  // 4
+#ifndef TAPER_ITEM_COST0
+#define TAPER_ITEM_COST0 0
+#endif
+constexpr int kItemCost0 = TAPER_ITEM_COST0;  // fixed per-item cost in the claim order
 constexpr double kEps = 1e-9;  // Alg. 1 line 16 "EPS" (no value in the paper) [C-adm-3]
 
 struct AdmitParams {
@@ -601,7 +605,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
           // group, so they stay adjacent in the claim order: claimed together, the later
           // group re-reads the chunk from L2 instead of HBM
           const int wr = (d.flags & 1) ? d.w : p.req_adm_off[d.r + 1] - p.req_adm_off[d.r];
-          const int cost = d.nt * (min(wr, kMaxItemBranches) > 4 ? 3 : 2);
+          const int cost = d.nt * (min(wr, kMaxItemBranches) > 4 ? 3 : 2) + kItemCost0;
           key = ((unsigned long long)(0xffff - cost) << 32) | (unsigned)i;
         }
         keys[i] = key;
