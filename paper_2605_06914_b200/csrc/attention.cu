@@ -798,6 +798,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       Item x;
       decode_item(recs + item_idx % kItemRing, x);
       ring_release(it_empty, item_idx, lane);
+#ifdef TAPER_TRACE_ITEMS
+      if (it < 0 && lane == 0 && p.trace != nullptr) {  // per-CTA items and tiles (debug)
+        p.trace[(size_t)(3000 + blockIdx.x) * 16 + 3] = item_idx;
+        p.trace[(size_t)(3000 + blockIdx.x) * 16 + 4] = n;
+      }
+#endif
       if (it < 0) break;
       const int wi = __shfl_sync(0xffffffffu, x.w, 0);
       const int nt = __shfl_sync(0xffffffffu, x.nt, 0);

@@ -53,6 +53,14 @@ def main():
     print("per-CTA (us): start min/max %.1f/%.1f, first TMA median %.1f, end min/median/max %.1f/%.1f/%.1f" % (
         (cta[:, 0].min() - g0) / 1e3, (cta[:, 0].max() - g0) / 1e3, np.median(cta[:, 2] - g0) / 1e3,
         (cta[:, 1].min() - g0) / 1e3, np.median(cta[:, 1] - g0) / 1e3, (cta[:, 1].max() - g0) / 1e3))
+    cta5 = tr.view(cap, 16).cpu().numpy()[3000:3000 + 148, :5].astype(np.int64)
+    if cta5[:, 4].any():  # built with -DTAPER_TRACE_ITEMS: items / tiles per CTA
+        end = (cta5[:, 1] - g0) / 1e3
+        o = np.argsort(end)
+        print("CTA end us / items / tiles, 10 earliest:", [(round(end[i], 1), int(cta5[i, 3]), int(cta5[i, 4])) for i in o[:10]])
+        print("10 latest:", [(round(end[i], 1), int(cta5[i, 3]), int(cta5[i, 4])) for i in o[-10:]])
+        print("tiles per CTA min/median/max", cta5[:, 4].min(), np.median(cta5[:, 4]), cta5[:, 4].max(),
+              "corr(end, tiles) %.2f" % np.corrcoef(end, cta5[:, 4])[0, 1])
     a = tr.view(cap, 16).cpu().numpy()
     np.save("gpurun_out/trace_raw.npy", a)
     n = int((a[:, 1] > 0).sum())
