@@ -19,7 +19,8 @@ def main():
     n_calls = int(sys.argv[3]) if len(sys.argv) > 3 else 32
     h = int(sys.argv[4]) if len(sys.argv) > 4 else 8  # KV heads of the rank (8 / G)
     b = synth.config_batch(cfg, seed=0)
-    lay = synth.make_layout(b, 64, np.random.default_rng(1), 1)
+    lay = synth.make_layout(b, 64, np.random.default_rng(1), 1,
+                            contiguous=os.environ.get("LAYOUT") == "contig")
     db = T.DeviceBatch.from_host(b)
     adm = T.DeviceAdmission.empty(b.n_req, b.n_slot)
     # 2x the h = 1 bound: room for experimental finer splits (TAPER_CHUNK_MIN variants)

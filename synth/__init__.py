@@ -154,7 +154,7 @@ def random_small_batch(rng, max_req=6, max_fanout=5, max_shared=4096, max_local=
 
 
 def make_layout(batch: Batch, page_size: int = PAGE, rng=None, spare_pages: int = 0,
-                local_capacity: int | None = None) -> Layout:
+                local_capacity: int | None = None, contiguous: bool = False) -> Layout:
     """Give every shared segment ceil(Lsh/page) pages and every slot's local segment
     ceil(max(Lloc, local_capacity)/page) pages, drawn as a random permutation of
     the pool (so segments are not contiguous).  A batch with local segments gets
@@ -178,7 +178,7 @@ def make_layout(batch: Batch, page_size: int = PAGE, rng=None, spare_pages: int 
         loc = np.maximum(loc, local_capacity)
     need_loc = (loc + page_size - 1) // page_size
     total = int(need_sh.sum() + need_loc.sum()) + spare_pages
-    perm = rng.permutation(max(total, 1)).astype(np.int32)
+    perm = (np.arange(max(total, 1)) if contiguous else rng.permutation(max(total, 1))).astype(np.int32)
     req_pages = perm[: need_sh.sum()]
     slot_pages = perm[need_sh.sum(): need_sh.sum() + need_loc.sum()]
     return Layout(page_size, max(total, 1), _csr(need_sh), np.ascontiguousarray(req_pages),
