@@ -219,6 +219,20 @@ TAPER_API int taper_decode_attention(const taper_batch *batch, const taper_admis
                            float scale, void *workspace, size_t workspace_bytes,
                            void *stream);
 
+/* Append the step's new token K/V of every admitted slot to the cache (Sec. 3.1,
+ * [C-att-3]: the current token is the last token of the slot's context).  Call after the
+ * lengths in `batch` include the new token and before taper_decode_attention:
+ *   * branch (Lloc_s >= 1): local position Lloc_s - 1 -- with local segments, the last
+ *     token of the last non-empty segment;
+ *   * serial request (Lloc_s = 0): shared position Lsh_r - 1.
+ *   k_new, v_new: bf16 [S, h_local, 128], slot-indexed (RoPE already applied to k_new).
+ * WRITES kv->k_pages / kv->v_pages (declared const for the attention call).  Slots with
+ * no position (Lsh_r + Lloc_s = 0) set TAPER_STATUS_BAD_LENGTH in adm->status.
+ * Errors: TAPER_ERR_ARG, _CAPACITY, _CUDA.                                              */
+TAPER_API int taper_append_kv(const taper_batch *batch, const taper_admission *adm,
+                              const taper_kv *kv, const void *k_new, const void *v_new,
+                              void *stream);
+
 /* Profiling hook (bench.py): when `events` is non-NULL, every later
  * taper_decode_attention call on this thread records events[0] before the shared-prefix
  * kernel, events[1] between it and the local/merge kernel and events[2] after, on the

@@ -24,6 +24,7 @@ TAPER_STATUS_PRECISION, TAPER_STATUS_WORK_OVERFLOW = 4, 8
 TAPER_MAX_SLOTS = 4096
 TAPER_CHUNK_TOKENS = 4096
 EXPORTS = ("taper_workspace_size", "taper_admit", "taper_build_work", "taper_decode_attention",
+           "taper_append_kv",
            "taper_status_string", "taper_last_error", "taper_last_launch_count",
            "taper_set_profile_events", "taper_set_trace_buffer")
 
@@ -75,6 +76,8 @@ def load_library() -> ctypes.CDLL:
                                      ctypes.c_size_t, _vp]
     lib.taper_decode_attention.argtypes = [P(_Batch), P(_Admission), P(_KV), _vp, _vp, _vp,
                                            ctypes.c_float, _vp, ctypes.c_size_t, _vp]
+    lib.taper_append_kv.argtypes = [P(_Batch), P(_Admission), P(_KV), _vp, _vp, _vp]
+    lib.taper_append_kv.restype = ctypes.c_int
     lib.taper_status_string.restype = ctypes.c_char_p
     lib.taper_status_string.argtypes = [ctypes.c_int]
     lib.taper_last_error.restype = ctypes.c_char_p
@@ -297,3 +300,13 @@ def taper_decode_attention(batch: DeviceBatch, adm: DeviceAdmission, kv: DeviceK
                                        _ptr(workspace),
                                        workspace.numel() * workspace.element_size(),
                                        _stream(stream)), "taper_decode_attention")
+
+
+def taper_append_kv(batch: DeviceBatch, adm: DeviceAdmission, kv: DeviceKV,
+                    k_new: torch.Tensor, v_new: torch.Tensor, stream=None):
+    """Write each admitted slot's new token K/V ([S, h_local, 128] bf16) into the pages."""
+    assert k_new.dtype == torch.bfloat16 and v_new.dtype == torch.bfloat16
+    assert k_new.is_contiguous() and v_new.is_contiguous()
+    bc, ac, kc = batch.c(), adm.c(), kv.c()
+    _check(_lib.taper_append_kv(ctypes.byref(bc), ctypes.byref(ac), ctypes.byref(kc),
+                                _ptr(k_new), _ptr(v_new), _stream(stream)), "taper_append_kv")

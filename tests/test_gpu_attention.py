@@ -224,3 +224,65 @@ def test_max_slots_capacity():
     es, eh = np.repeat(slots, 2), np.tile([5, 60], len(slots))
     ref, ref_lse = case.run_oracle(es, eh)
     assert_close(out[es, eh].float().numpy(), ref, "max slots")
+
+
+# ------------------------------------------------------------ KV append of the current token
+@pytest.mark.parametrize("segmented", [False, True])
+def test_append_kv_places_current_token(segmented):
+    """taper_append_kv writes each ADMITTED slot's new K/V row at the last position of its
+    context ([C-att-3]): last local token (last non-empty segment) for a branch, last shared
+    token for a serial request; every other pool row is untouched, and the attention that
+    follows matches the oracle on the updated cache."""
+    from paper_2605_06914_b200 import taper as T
+    rng = np.random.default_rng(41)
+    b = synth.make_batch([70, 5, 130, 64], [1, 2, 2, 1], [0, 3, 64, 9, 1, 0], 1e3, 0.0, rng=rng)
+    if segmented:
+        b = synth.with_segments(b, [[], [1, 2], [64], [4, 5, 0], [1], []])
+    b.req_slack_ms[:] = 1e3
+    case = Case(b, page=16, seed=2)
+    lay, ps = case.layout, 16
+    dev = "cuda"
+    db = T.DeviceBatch.from_host(b, dev)
+    adm = T.DeviceAdmission.empty(b.n_req, b.n_slot, dev)
+    ws = torch.empty(T.taper_workspace_size(b.n_req, b.n_slot, 8, 64), dtype=torch.uint8, device=dev)
+    T.taper_admit(db, (1.0, 0.1, 1e-3), "off", 0.8, adm, 8, ws)  # protected slots only
+    rpo, rp, spo, sp = T.page_tables_to_device(lay, dev)
+    spg = None if lay.seg_page_off is None else \
+        torch.as_tensor(np.concatenate([lay.seg_page_off, [0]]).astype(np.int32)).to(dev)
+    k0, v0 = case.k.clone(), case.v.clone()
+    kd, vd = case.k.to(dev), case.v.to(dev)
+    kv = T.DeviceKV(kd, vd, rpo, rp, spo, sp, spg)
+    g = torch.Generator().manual_seed(5)
+    kn = torch.randn((b.n_slot, 8, 128), generator=g).bfloat16()
+    vn = torch.randn((b.n_slot, 8, 128), generator=g).bfloat16()
+    T.taper_append_kv(db, adm, kv, kn.to(dev), vn.to(dev))
+    torch.cuda.synchronize()
+    assert int(adm.status.item()) == 0
+    mask = adm.slot_admitted.cpu().numpy()[:b.n_slot].astype(bool)
+    assert 0 < mask.sum() < b.n_slot
+    exp_k, exp_v = k0.clone(), v0.clone()
+    off = b.req_slot_off
+    for s in np.flatnonzero(mask):  # expected position, test-side
+        r = int(np.searchsorted(off, s, side="right") - 1)
+        if b.slot_local_len[s] > 0:
+            if segmented:
+                segs = [q for q in range(b.slot_seg_off[s], b.slot_seg_off[s + 1]) if b.seg_len[q] > 0]
+                q = segs[-1]
+                t = int(b.seg_len[q]) - 1
+                page = lay.slot_pages[lay.seg_page_off[q] + t // ps]
+            else:
+                t = int(b.slot_local_len[s]) - 1
+                page = lay.slot_pages[lay.slot_page_off[s] + t // ps]
+        else:
+            t = int(b.req_shared_len[r]) - 1
+            page = lay.req_pages[lay.req_page_off[r] + t // ps]
+        exp_k[page, :, t % ps] = kn[s]
+        exp_v[page, :, t % ps] = vn[s]
+    assert torch.equal(kd.cpu(), exp_k) and torch.equal(vd.cpu(), exp_v)
+    # the step's attention on the updated cache
+    case.k, case.v = exp_k, exp_v
+    q = case.q.to(dev)
+    out = torch.full_like(q, float("nan"))
+    T.taper_decode_attention(db, adm, kv, q, out, None, case.scale, ws)
+    torch.cuda.synchronize()
+    _check_all(case, adm, out.cpu(), None, heads=[0, 21, 63], what="after append")
