@@ -602,11 +602,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     p.trace[(size_t)(3000 + blockIdx.x) * 16 + 0] = (long long)g;
   }
 
+#ifndef TAPER_NO_ZERO_FILL
   // Zero the K/V rings once: token rows of a partial tile that TMA does not load must hold
   // finite values (P = 0 there, but 0 * NaN would still poison O).
   for (int i = tid; i < kOffQ / 16; i += kAttnThreads)
     reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
   fence_proxy_async_smem();
+#endif
   if (tid == 0) {
     for (int i = 0; i < kKStages; ++i) { mbar_init(kfull + i, 1); mbar_init(kempty + i, 1); }
     for (int i = 0; i < kVStages; ++i) { mbar_init(vfull + i, 1); mbar_init(vempty + i, 1); }
