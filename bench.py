@@ -187,6 +187,13 @@ def cpu_baseline(batch, layout, adm_mask, seconds, seed, layers):
             "admit_ms": t_admit * 1e3, "step_s_extrapolated": t_step}
 
 
+def _barrier(dist, local):
+    if os.environ.get("TAPER_BENCH_BACKEND", "nccl") == "nccl":
+        dist.barrier(device_ids=[local])
+    else:
+        dist.barrier()
+
+
 def build_batch(args):
     if args.config == "reduce":
         return synth.reduce_batch(seed=args.seed, slack_min_ms=1e6)
@@ -247,10 +254,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TAPER_BENCH_BACKEND=gloo (dev only): exercise the multi-rank path with several ranks on
+    # one GPU (NCCL needs one GPU per rank); never used for a reported number
+    backend = os.environ.get("TAPER_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     G = world
     assert 8 % G == 0, "KV heads (8) must divide evenly across GPUs"
     h = 8 // G
@@ -327,7 +342,7 @@ def run_ours(args):
 
     def barrier():
         if G > 1:
-            dist.barrier(device_ids=[local])
+            _barrier(dist, local)
         torch.cuda.synchronize(dev)
 
     for _ in range(max(3, args.warmup)):
@@ -418,7 +433,7 @@ def run_ours(args):
                                 f"one rank of a kv-head shard x{args.rank_of} (per-rank work, "
                                 "no collectives; value = that rank's steps/s)"),
                 "l2": f"inputs larger than L2 ({layer_bytes / 1e9:.2f} GB K/V per layer per GPU)",
-                "step": "admit + 64 x decode_attention (+ bcast/all-gather when G>1); no FFN",
+                "step": f"admit + {L} x decode_attention (+ bcast/all-gather when G>1); no FFN",
             },
             "attn_gbs_per_gpu": attn_gbs, "step_hbm_gbs_total": step_gbs,
             "attn_frac_of_measured_hbm": attn_gbs / hbm_peak,
@@ -445,7 +460,7 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     if G > 1:
-        dist.barrier(device_ids=[local])
+        _barrier(dist, local)
         dist.destroy_process_group()
 
 
@@ -515,7 +530,7 @@ def run_e2e(args, T, torch, dist, G, batch, db, adm, ws, kvs, L, S, h, scale, de
         e2e_step()
     torch.cuda.synchronize(dev)
     if G > 1:
-        dist.barrier(device_ids=[local])
+        _barrier(dist, local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n = max(3, args.steps // 2)
     e0.record(comp)
