@@ -192,6 +192,8 @@ __device__ void greedy_literal(const AdmitParams &p, const unsigned long long *k
     if (r < R) p.req_part_off[r] = cnt[k];  // scratch: rewritten by the work-list pass
   }
   __syncthreads();
+  // one request per thread while R <= 1024 (the fp64 division chain per candidate is the
+  // iteration's latency, so candidates are spread over threads, not stacked per thread)
   const int nwarps = min(kAdmitThreads / 32, max(1, (R + 31) / 32));
   const int nthr = nwarps * 32;
   if (tid < nthr) {
@@ -225,12 +227,21 @@ __device__ void greedy_literal(const AdmitParams &p, const unsigned long long *k
         if (better(score, r, b.score, b.r)) { b.score = score; b.dL = dL; b.r = r; }
       }
       b = warp_argmax(b);
-      const int buf = it & 1;
-      if (lane == 0) { wb_score[buf][tid >> 5] = b.score; wb_dL[buf][tid >> 5] = b.dL; wb_r[buf][tid >> 5] = b.r; }
-      asm volatile("bar.sync 1, %0;" :: "r"(nthr) : "memory");
-      Best w{0.0, 0, -1};
-      if (lane < nwarps) { w.score = wb_score[buf][lane]; w.dL = wb_dL[buf][lane]; w.r = wb_r[buf][lane]; }
-      w = warp_argmax(w);
+      Best w = b;
+      if (nwarps > 1) {
+        const int buf = it & 1;
+        if (lane == 0) { wb_score[buf][tid >> 5] = b.score; wb_dL[buf][tid >> 5] = b.dL; wb_r[buf][tid >> 5] = b.r; }
+        asm volatile("bar.sync 1, %0;" :: "r"(nthr) : "memory");
+        w = Best{0.0, 0, -1};
+        if (nwarps <= 2) {  // two warps: a broadcast scan beats five shuffle rounds (measured)
+          for (int j = 0; j < nwarps; ++j)
+            if (better(wb_score[buf][j], wb_r[buf][j], w.score, w.r))
+              w = Best{wb_score[buf][j], wb_dL[buf][j], wb_r[buf][j]};
+        } else {
+          if (lane < nwarps) { w.score = wb_score[buf][lane]; w.dL = wb_dL[buf][lane]; w.r = wb_r[buf][lane]; }
+          w = warp_argmax(w);
+        }
+      }
       if (w.r < 0 || w.score <= 0.0) break;  // L21-22: no feasible increment of value
       n += 1; L += w.dL;                         // L23-26: commit
 #pragma unroll
