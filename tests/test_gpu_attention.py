@@ -286,3 +286,21 @@ def test_append_kv_places_current_token(segmented):
     T.taper_decode_attention(db, adm, kv, q, out, None, case.scale, ws)
     torch.cuda.synchronize()
     _check_all(case, adm, out.cpu(), None, heads=[0, 21, 63], what="after append")
+
+
+@pytest.mark.parametrize("heads", [(0, 3), (3, 8), (2, 7)])
+def test_odd_head_counts(heads):
+    """h_local need not divide 8 (the C ABI takes 1..8 heads): 3- and 5-head slices at an
+    arbitrary head offset match the oracle (prefix split taper_chunk_tokens(Lsh, h))."""
+    rng = np.random.default_rng(3)
+    b = synth.make_batch([5000, 700, 64], [3, 1, 2], rng.integers(1, 200, 6).tolist(), 1e3, 0.0,
+                         rng=rng)
+    case = Case(b, page=64, seed=12)
+    adm, out, lse = case.run_gpu(policy="eager", heads=heads)
+    g0, g1 = heads
+    sub = np.arange(8 * g0, 8 * g1)
+    adm_slots = np.flatnonzero(adm.slot_admitted.cpu().numpy()[:b.n_slot])
+    es, eh = np.meshgrid(adm_slots, np.arange(len(sub)), indexing="ij")
+    es, eh = es.ravel(), eh.ravel()
+    ref, _ = case.run_oracle(es, sub[eh])
+    assert_close(out[es, eh].float().numpy(), ref, f"heads {heads}")
