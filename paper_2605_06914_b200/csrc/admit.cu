@@ -23,6 +23,13 @@ constexpr int kPerThread = kMaxSlots / kAdmitThreads;  // 4
 #define TAPER_ITEM_COST0 0
 #endif
 constexpr int kItemCost0 = TAPER_ITEM_COST0;  // fixed per-item cost in the claim order
+#ifndef TAPER_WIDE_COST
+#define TAPER_WIDE_COST 3
+#endif
+#ifndef TAPER_NARROW_COST
+#define TAPER_NARROW_COST 2
+#endif
+constexpr int kWideCost = TAPER_WIDE_COST, kNarrowCost = TAPER_NARROW_COST;  // per tile
 constexpr double kEps = 1e-9;  // Alg. 1 line 16 "EPS" (no value in the paper) [C-adm-3]
 
 struct AdmitParams {
@@ -616,7 +623,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
           // group, so they stay adjacent in the claim order: claimed together, the later
           // group re-reads the chunk from L2 instead of HBM
           const int wr = (d.flags & 1) ? d.w : p.req_adm_off[d.r + 1] - p.req_adm_off[d.r];
-          const int cost = d.nt * (min(wr, kMaxItemBranches) > 4 ? 3 : 2) + kItemCost0;
+          const int cost = d.nt * (min(wr, kMaxItemBranches) > 4 ? kWideCost : kNarrowCost) + kItemCost0;
           key = ((unsigned long long)(0xffff - cost) << 32) | (unsigned)i;
         }
         keys[i] = key;
