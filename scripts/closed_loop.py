@@ -53,6 +53,8 @@ class Req:
     max_gap: float = 0.0
     tokens: int = 0
     done: bool = False
+    segs: list = None      # reduce stage: finished branches' lengths (canonical order)
+    z: int = 0             # reduce tokens so far (the last local segment)
 
     def start_stage(self):
         while self.stages:
@@ -91,18 +93,25 @@ def arrival_rate(step, n_steps):
 
 
 def batch_of(active, now):
-    shared, fan, loc, slack = [], [], [], []
+    """A reduce-stage request is one slot whose local context is its finished branches in
+    canonical order plus z, each segment in its own pages (Sec. 3.1):
+    nothing is copied when a phase ends."""
+    shared, fan, segs, slack = [], [], [], []
     for r in active:
         shared.append(r.lsh)
         if r.branches:
             live = [b for b in r.branches if b[0] < b[1]]
             fan.append(len(live))
-            loc += [b[0] for b in live]
+            segs += [[b[0]] for b in live]
+        elif r.segs is not None:
+            fan.append(1)
+            segs.append(r.segs + [r.z])
         else:
             fan.append(1)
-            loc.append(0)
+            segs.append([])
         slack.append(r.last_progress + SLO_MS - now)
-    b = synth.make_batch(shared, fan, loc, 0.0, 0.0)
+    b = synth.make_batch(shared, fan, [sum(x) for x in segs], 0.0, 0.0)
+    b = synth.with_segments(b, segs)
     b.req_slack_ms = np.asarray(slack, np.float64)
     return b
 
@@ -124,11 +133,15 @@ def advance(active, b, slot_admitted, now):
                     x[0] += 1
                     toks += 1
             if all(x[0] >= x[1] for x in r.branches):  # phase complete -> reduce context
-                r.lsh += sum(x[0] for x in r.branches)
+                r.segs = [x[0] for x in r.branches]       # read in place, not copied
+                r.z = 0
                 r.branches = []
                 r.start_stage()
         else:
-            r.lsh += 1
+            if r.segs is not None:
+                r.z += 1      # reduce token: appended to the last local segment
+            else:
+                r.lsh += 1
             r.serial_left -= 1
             toks += 1
             if r.serial_left <= 0:
@@ -263,7 +276,8 @@ def gpu_drivers(timed_layers):
         lay = synth.make_layout(b, 64, np.random.default_rng(len(b.slot_local_len)))
         assert lay.num_pages <= pool_pages, lay.num_pages
         rpo, rp, spo, sp = T.page_tables_to_device(lay)
-        kv = T.DeviceKV(k, v, rpo, rp, spo, sp)
+        spg = torch.as_tensor(np.concatenate([lay.seg_page_off, [0]]).astype(np.int32)).cuda()
+        kv = T.DeviceKV(k, v, rpo, rp, spo, sp, spg)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         sc = 1 / math.sqrt(128)
         T.taper_decode_attention(state["db"], state["adm"], kv, q, out, None, sc, ws)  # warm
