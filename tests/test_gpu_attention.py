@@ -304,3 +304,20 @@ def test_odd_head_counts(heads):
     es, eh = es.ravel(), eh.ravel()
     ref, _ = case.run_oracle(es, sub[eh])
     assert_close(out[es, eh].float().numpy(), ref, f"heads {heads}")
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_full_size_one_rank_of_8_sampled(name):
+    """BASELINE.json configs[2] / [4] at full size as one rank of the 8-GPU KV-head shard
+    (h_local = 1, the launch configuration `bench.py --rank-of 8` times): sampled admitted
+    slots x all 8 local Q heads against the oracle."""
+    b = synth.config_batch(name, seed=1)
+    case = Case(b, h_kv=1, seed=1)
+    adm, out, lse = case.run_gpu(policy="eager")
+    rng = np.random.default_rng(1)
+    slots = np.sort(rng.choice(np.flatnonzero(adm.slot_admitted.cpu().numpy()[:b.n_slot]), 24,
+                               replace=False))
+    es, eh = np.repeat(slots, 8), np.tile(np.arange(8), len(slots))
+    ref, ref_lse = case.run_oracle(es, eh)
+    assert_close(out[es, eh].float().numpy(), ref, f"{name} rank of 8")
+    np.testing.assert_allclose(lse[es, eh].numpy(), ref_lse, atol=2e-3, rtol=1e-4)
