@@ -8,10 +8,12 @@
 //  A6+A7  attend_kernel (tcgen05 + TMA, one persistent CTA per SM, dynamic scheduling)
 //     Work items of one request r and local KV head g; the stacked query operand is
 //     Q^T = [8 GQA heads] x [w admitted branches] (N = 8 w <= 64 rows):
-//       * shared item : one 4096-token chunk of P (+) H for a group of <= 8 admitted
+//       * shared item : one chunk of P (+) H (taper_chunk_tokens(Lsh, h) <= 4096 tokens,
+//                       include/taper.h) for a group of <= 8 admitted
 //                       branches -- every page read ONCE from HBM and contracted against
 //                       all stacked rows (the cascade);
-//       * local item  : <= 16 64-token tiles of ONE admitted branch's h_i (+) y_i (w = 1).
+//       * local item  : <= 16 64-token tiles of ONE admitted branch's h_i (+) y_i (w = 1),
+//                       or of one local segment of a reduce step's context (L104-107).
 //     Per 64-token tile, "swap-AB" (tokens on the MMA's M, stacked rows on N):
 //       S^T = K Q^T    tcgen05.mma SS, M = 64 tokens, N = 8 w, K = 128 (A = the K tile by
 //                      TMA, B = Q^T by TMA, both SMEM; fp32 S^T in TMEM)

@@ -12,7 +12,7 @@ namespace taper {
 
 constexpr int kHeadDim = TAPER_HEAD_DIM;
 constexpr int kGroup = TAPER_GQA_GROUP;
-constexpr int kChunk = TAPER_CHUNK_TOKENS;
+constexpr int kChunk = TAPER_CHUNK_TOKENS;  // largest prefix chunk (taper_chunk_tokens)
 constexpr int kMaxSlots = TAPER_MAX_SLOTS;
 constexpr int kTileTokens = 64;       // tokens per pipeline tile (one TMA stage)
 constexpr int kLocalItemTiles = 16;   // branch-local tiles per local work item
