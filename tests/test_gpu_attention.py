@@ -321,3 +321,28 @@ def test_full_size_one_rank_of_8_sampled(name):
     ref, ref_lse = case.run_oracle(es, eh)
     assert_close(out[es, eh].float().numpy(), ref, f"{name} rank of 8")
     np.testing.assert_allclose(lse[es, eh].numpy(), ref_lse, atol=2e-3, rtol=1e-4)
+
+
+def test_branch_isolation_and_wide_schedule_invariance_bitwise():
+    """Sec. 3.1 visibility rule / Lemma 1 on the GPU, bitwise: (a) perturbing the local KV of
+    a slot's siblings leaves its output bits unchanged; (b) a 14-branch request admitted at
+    width 14 (two branch groups of one chunk) or width 5 (one group) gives the common slots
+    identical bits."""
+    rng = np.random.default_rng(17)
+    b = synth.make_batch([5000, 300], [14, 1], rng.integers(1, 300, 14).tolist() + [0], 1e3, 0.0,
+                         rng=rng)
+    case = Case(b, seed=4)
+    adm_e, out_e, _ = case.run_gpu(policy="eager", with_lse=False)
+    adm_c, out_c, _ = case.run_gpu(policy="cap", cap=5, with_lse=False)
+    both = (adm_e.slot_admitted.cpu().numpy()[:b.n_slot] & adm_c.slot_admitted.cpu().numpy()[:b.n_slot]).astype(bool)
+    assert both.sum() == 6
+    assert torch.equal(out_e[both], out_c[both])
+    # (a) perturb every sibling of slot 0 in its own local pages
+    lay = case.layout
+    for s in range(1, 14):
+        for pg in lay.slot_pages[lay.slot_page_off[s]:lay.slot_page_off[s + 1]]:
+            case.k[pg] = (case.k[pg].float() + 3.0).bfloat16()
+            case.v[pg] = (case.v[pg].float() - 5.0).bfloat16()
+    _, out_p, _ = case.run_gpu(policy="eager", with_lse=False)
+    assert torch.equal(out_p[0], out_e[0])
+    assert not torch.equal(out_p[1], out_e[1])
