@@ -139,6 +139,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
+#if defined(TAPER_POLL_NS) && TAPER_POLL_NS > 0
+    __nanosleep(TAPER_POLL_NS);  // experiment: back off between polls (power-capped runs)
+#endif
     if (clock64() - t0 > (1ll << 35)) __trap();  // ~17 s at 2 GHz
   }
 }
