@@ -154,10 +154,12 @@ def test_utility_config_batches(kind):
             _compare(b, (12.0, 0.03, 2e-5), "taper", 0.8, utility=util)
 
 
-def test_utility_max_capacity():
+@pytest.mark.parametrize("R", [1024, 2048])
+def test_utility_max_capacity(R):
+    """4096 slots; R = 2048 gives every admission thread two requests (kOwn > 1)."""
     rng = np.random.default_rng(17)
-    fan = np.full(1024, 4)
-    b = synth.make_batch(rng.integers(0, 32768, 1024), fan, rng.integers(0, 512, 4096), 40.0, 20.0,
+    fan = np.full(R, 4096 // R)
+    b = synth.make_batch(rng.integers(0, 32768, R), fan, rng.integers(0, 512, 4096), 40.0, 20.0,
                          rng=rng)
     util = synth.utility_table(rng, b.n_req, 4, "concave")
     _compare(b, (12.0, 0.03, 2e-5), "taper", 0.8, utility=util)
