@@ -142,7 +142,7 @@ __device__ __forceinline__ double warp_min_d(double x) {
   return x;
 }
 
-// u_r(k) of the caller's table, flat past its last column (as the oracle reads it)
+// u_r(k) of the caller's table, flat past its last column (reading R-util)
 __device__ __forceinline__ double util_at(const AdmitParams &p, int r, int k) {
   return p.util[(long long)r * p.ustride + min(k, p.ustride - 1)];
 }

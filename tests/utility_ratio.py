@@ -1,7 +1,7 @@
 """Greedy / optimum utility ratio of Alg. 1 under operator utilities (SURVEY 8(f) NEXT-3,
 reading C-adm-12).  Oracle only (literal Alg. 1 vs App. B brute force) on tiny random
 batches; prints min / mean / share of instances below 1 and below 1/2 per utility kind.
-usage: python scripts/utility_ratio.py [instances]"""
+usage: python tests/utility_ratio.py [instances]  (test infrastructure: it runs the oracle)"""
 import os
 import sys
 
