@@ -71,6 +71,30 @@ __device__ __forceinline__ int local_items(const AdmitParams &p, int s) {
   return n;
 }
 
+// Prefix chunks of a request (a function of Lsh and h_local only: schedule invariance,
+// Lemma 1).  Nominal chunks of ck = taper_chunk_tokens(Lsh, h) tokens; with >= 3 chunks and
+// TAPER_SKEW_CHUNKS, the first is ck + ck/2 and the others shift by ck/2, so the last one is
+// about half a chunk: the longest-first claim order then ends on short items.  Chunk starts
+// stay multiples of 64 tokens (a tile never straddles a page).
+#ifndef TAPER_SKEW_CHUNKS
+#define TAPER_SKEW_CHUNKS 0
+#endif
+struct ChunkPlan { int ck, half, n; bool skew; };
+__device__ __forceinline__ ChunkPlan chunk_plan(int lsh, int h) {
+  ChunkPlan c;
+  c.ck = taper_chunk_tokens(lsh, h);
+  c.half = (c.ck / 2) / kTileTokens * kTileTokens;
+  const int n = (lsh + c.ck - 1) / c.ck;
+  c.skew = TAPER_SKEW_CHUNKS && n >= 3 && c.ck + c.half <= kChunk;
+  c.n = (c.skew && (n - 1) * c.ck + c.half >= lsh) ? n - 1 : n;
+  return c;
+}
+__device__ __forceinline__ int chunk_start(const ChunkPlan &c, int lsh, int i) {
+  if (i >= c.n) return lsh;
+  if (!c.skew || i == 0) return min(i * c.ck, lsh);
+  return min(i * c.ck + c.half, lsh);
+}
+
 __device__ __forceinline__ double T_eval(double a, double b, double c, long long n,
                                          long long L) {
   // App. C.1: T(S) = a + b*n_tokens + c*L_context, each operation rounded separately.
@@ -477,10 +501,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
             w += 1;
             nl += local_items(p, s);
           }
-        if (w > 0 && p.Lsh[r] > 0) {
-          const int ck = taper_chunk_tokens(p.Lsh[r], p.h_local);
-          nc = (p.Lsh[r] + ck - 1) / ck;
-        }
+        if (w > 0 && p.Lsh[r] > 0) nc = chunk_plan(p.Lsh[r], p.h_local).n;
       }
       p.req_width[r] = w;
     }
@@ -535,7 +556,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     const int nc = nsh / groups;
     const int cs_r = p.req_part_off[r];
     const int it0 = p.req_chunk_off[r] + p.req_loc_off[r];  // request-major item numbering
-    const int ck = taper_chunk_tokens(p.Lsh[r], p.h_local);  // include/taper.h
+    const ChunkPlan cp = chunk_plan(p.Lsh[r], p.h_local);
     for (int c = 0; c < nc; ++c)
       for (int g = 0; g < groups; ++g) {
         ItemDesc d;
@@ -543,7 +564,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
         d.w = min(kMaxItemBranches, w - g * kMaxItemBranches);
         d.adm_off = adm_off + g * kMaxItemBranches;
         d.cs0 = cs_r + c * w + g * kMaxItemBranches;
-        d.tb = c * ck; d.te = min(d.tb + ck, p.Lsh[r]);
+        d.tb = chunk_start(cp, p.Lsh[r], c); d.te = chunk_start(cp, p.Lsh[r], c + 1);
         d.nt = (d.te - d.tb + kTileTokens - 1) / kTileTokens;
         d.flags = 0;
         p.items[it0 + c * groups + g] = d;
