@@ -42,11 +42,18 @@ def main():
     for i in range(n_pools):
         T.taper_decode_attention(db, adm, pools[i], q, out, None, sc, ws)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # INTERLEAVE=1: a foreign kernel between calls (as the projections / MLP of a real layer
+    # would be), so the attend prologue cannot overlap the previous merge via PDL; the tiny
+    # kernel's own time (~2 us) is included
+    inter = os.environ.get("INTERLEAVE") == "1"
+    dummy = torch.zeros(1024, device="cuda")
     ts = []
     for rep in range(5):
         e0.record()
         for i in range(n_calls):
             T.taper_decode_attention(db, adm, pools[i % n_pools], q, out, None, sc, ws)
+            if inter:
+                dummy.add_(1.0)
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) / n_calls * 1e3)
