@@ -58,7 +58,7 @@ struct AdmitParams {
   int h_local;
   ItemDesc *items;   // [cap_cs] work items (A5)
   int4 *ltiles;      // [cap_cs * 16] local tiles {slot, tok0, valid, jrow}
-  int32_t *order;    // [cap_cs] claim order of the items (longest first)
+  ItemDesc *sorted;  // [cap_cs] the item descriptors in claim order (longest first)
 };
 
 // Local work items of slot s: one per <= kLocalItemTiles 64-token tiles of each of its
@@ -651,9 +651,9 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       }
       __syncthreads();
       bitonic_sort(keys, n_keys);
-      for (int i = tid; i < D; i += blockDim.x) p.order[i] = int(keys[i] & 0xffffffffu);
+      for (int i = tid; i < D; i += blockDim.x) p.sorted[i] = p.items[int(keys[i] & 0xffffffffu)];
     } else {
-      for (int i = tid; i < D; i += blockDim.x) p.order[i] = i;
+      for (int i = tid; i < D; i += blockDim.x) p.sorted[i] = p.items[i];
     }
   }
   if (tid == 0) {
@@ -744,7 +744,7 @@ static int launch_admit(const taper_batch *batch, const taper_latency_model *mod
   p.cap_cs = T.cap_cs;
   p.items = reinterpret_cast<ItemDesc *>(w + T.items);
   p.ltiles = reinterpret_cast<int4 *>(w + T.ltiles);
-  p.order = reinterpret_cast<int32_t *>(w + T.order);
+  p.sorted = reinterpret_cast<ItemDesc *>(w + T.sorted);
   p.h_local = h_local;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (S > 0) {

@@ -103,7 +103,7 @@ struct AttnParams {
   const int32_t *adm_by_req;
   int32_t *done;       // [r * 8 + g]: items of (request, KV head) whose partials are written
   const ItemDesc *items;
-  const int32_t *order;  // claim order of the item descriptors (admit: longest first)
+  const ItemDesc *sorted;  // the item descriptors in claim order (admit: longest first)
   const int4 *ltiles;
   float *part_lse, *part_o;
   int h_local, page_size;
@@ -677,8 +677,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (it >= 0) {
         const int qi = it / h;  // claim index -> descriptor (longest first), then KV head
         g = it - qi * h;
-        const int q = __ldg(p.order + qi);
-        const int32_t d = lane < 8 ? __ldg(reinterpret_cast<const int32_t *>(p.items + q) + lane) : 0;
+        const int32_t d = lane < 8 ? __ldg(reinterpret_cast<const int32_t *>(p.sorted + qi) + lane) : 0;
         const int nt = __shfl_sync(0xffffffffu, d, 6);
         Item x;
         x.r = __shfl_sync(0xffffffffu, d, 0);
@@ -1258,7 +1257,7 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   ap.adm_by_req = reinterpret_cast<const int32_t *>(w + L.adm_by_req);
   ap.items = reinterpret_cast<const ItemDesc *>(w + tabs.items);
   ap.ltiles = reinterpret_cast<const int4 *>(w + tabs.ltiles);
-  ap.order = reinterpret_cast<const int32_t *>(w + tabs.order);
+  ap.sorted = reinterpret_cast<const ItemDesc *>(w + tabs.sorted);
   ap.part_lse = reinterpret_cast<float *>(w + tabs.lse);
   ap.part_o = reinterpret_cast<float *>(w + tabs.o);
   ap.h_local = h;

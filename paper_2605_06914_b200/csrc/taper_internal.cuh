@@ -63,7 +63,7 @@ __host__ __device__ inline WsLayout ws_layout(int R, int S) {
 constexpr size_t kPartBytesPerCsHead = size_t(kGroup) * (kHeadDim + 1) * sizeof(float);
 constexpr size_t kItemDescBytes = 32;                 // ItemDesc
 constexpr size_t kLocalTileBytes = 16;                // int4 {slot, tok0, valid, jrow}
-constexpr size_t kWorkBytesPerCs = kItemDescBytes + kLocalItemTiles * kLocalTileBytes + 4;
+constexpr size_t kWorkBytesPerCs = kItemDescBytes + kLocalItemTiles * kLocalTileBytes + kItemDescBytes;
 
 // Work item descriptor emitted by the admission kernel (A5).  Items are numbered per KV
 // head, request-major: request r's prefix chunks, then its local items.
@@ -87,7 +87,7 @@ __host__ __device__ inline int64_t ws_cap_cs(size_t bytes, int R, int S, int h_l
 // part_lse, part_o (partial row prow = ((cs * h_local + g) * 8 + qh)), item descriptors,
 // local-tile descriptors
 struct WsTables {
-  size_t lse, o, items, ltiles, order;
+  size_t lse, o, items, ltiles, sorted;  // sorted: the item descriptors in claim order
   int64_t cap_cs;
 };
 __host__ __device__ inline WsTables ws_tables(size_t bytes, int R, int S, int h_local) {
@@ -98,7 +98,7 @@ __host__ __device__ inline WsTables ws_tables(size_t bytes, int R, int S, int h_
   t.o = ws_align(t.lse + size_t(t.cap_cs) * h_local * kGroup * sizeof(float));
   t.items = ws_align(t.o + size_t(t.cap_cs) * h_local * kGroup * kHeadDim * sizeof(float));
   t.ltiles = ws_align(t.items + size_t(t.cap_cs) * kItemDescBytes);
-  t.order = ws_align(t.ltiles + size_t(t.cap_cs) * kLocalItemTiles * kLocalTileBytes);
+  t.sorted = ws_align(t.ltiles + size_t(t.cap_cs) * kLocalItemTiles * kLocalTileBytes);
   return t;
 }
 
