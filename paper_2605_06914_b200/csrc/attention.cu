@@ -102,7 +102,6 @@ struct AttnParams {
   int32_t *hdr;        // hdr[8]: work counter, hdr[9]: CTAs exited
   const int32_t *adm_by_req;
   int32_t *done;       // [r * 8 + g]: items of (request, KV head) whose partials are written
-  const ItemDesc *items;
   const ItemDesc *sorted;  // the item descriptors in claim order (admit: longest first)
   const int4 *ltiles;
   float *part_lse, *part_o;
@@ -1255,7 +1254,6 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   ap.hdr = reinterpret_cast<int32_t *>(w + L.hdr);
   ap.done = reinterpret_cast<int32_t *>(w + L.done);
   ap.adm_by_req = reinterpret_cast<const int32_t *>(w + L.adm_by_req);
-  ap.items = reinterpret_cast<const ItemDesc *>(w + tabs.items);
   ap.ltiles = reinterpret_cast<const int4 *>(w + tabs.ltiles);
   ap.sorted = reinterpret_cast<const ItemDesc *>(w + tabs.sorted);
   ap.part_lse = reinterpret_cast<float *>(w + tabs.lse);
