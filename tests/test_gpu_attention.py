@@ -346,3 +346,49 @@ def test_branch_isolation_and_wide_schedule_invariance_bitwise():
     _, out_p, _ = case.run_gpu(policy="eager", with_lse=False)
     assert torch.equal(out_p[0], out_e[0])
     assert not torch.equal(out_p[1], out_e[1])
+
+
+def test_build_work_from_broadcast_mask_matches_admit():
+    """G > 1 path: every rank rebuilds its work list from rank 0's
+    broadcast slot mask with taper_build_work.  From the mask alone it must reproduce
+    taper_admit's adm_list / n_adm / widths and give bitwise the same attention output, also
+    for a mask no policy of this batch would produce."""
+    from paper_2605_06914_b200 import taper as T
+    b = synth.config_batch("c2", seed=6, slack_min_ms=30.0)
+    case = Case(b, seed=6)
+    dev = "cuda"
+    db = T.DeviceBatch.from_host(b, dev)
+    ws = torch.empty(T.taper_workspace_size(b.n_req, b.n_slot, 8, T.max_chunk_slots(
+        b.req_shared_len, b.req_slot_off, b.slot_local_len)), dtype=torch.uint8, device=dev)
+    rpo, rp, spo, sp = T.page_tables_to_device(case.layout, dev)
+    kv = T.DeviceKV(case.k.to(dev), case.v.to(dev), rpo, rp, spo, sp)
+    q = case.q.to(dev)
+    adm = T.DeviceAdmission.empty(b.n_req, b.n_slot, dev)
+    T.taper_admit(db, (12.0, 0.03, 2e-5), "taper", 0.8, adm, 8, ws)
+    out1 = torch.full_like(q, float("nan"))
+    T.taper_decode_attention(db, adm, kv, q, out1, None, case.scale, ws)
+    # a second admission object holding only the mask, as after ncclBroadcast
+    adm2 = T.DeviceAdmission.empty(b.n_req, b.n_slot, dev)
+    adm2.slot_admitted.copy_(adm.slot_admitted)
+    ws.zero_()
+    T.taper_build_work(db, adm2, 8, ws)
+    out2 = torch.full_like(q, float("nan"))
+    T.taper_decode_attention(db, adm2, kv, q, out2, None, case.scale, ws)
+    torch.cuda.synchronize()
+    n = int(adm.n_adm.item())
+    assert 0 < n < b.n_slot and int(adm2.n_adm.item()) == n
+    assert torch.equal(adm.adm_list[:n], adm2.adm_list[:n])
+    assert torch.equal(adm.req_width, adm2.req_width)
+    m = adm.slot_admitted.bool()[:b.n_slot].cpu()
+    assert torch.equal(out1.cpu()[m], out2.cpu()[m])
+    # an arbitrary mask (every request keeps >= 1 slot): parity with the oracle
+    rng = np.random.default_rng(2)
+    mask = (rng.random(b.n_slot) < 0.5).astype(np.uint8)
+    mask[b.req_slot_off[:-1]] = 1
+    adm3 = T.DeviceAdmission.empty(b.n_req, b.n_slot, dev)
+    adm3.slot_admitted.copy_(torch.as_tensor(mask))
+    T.taper_build_work(db, adm3, 8, ws)
+    out3 = torch.full_like(q, float("nan"))
+    T.taper_decode_attention(db, adm3, kv, q, out3, None, case.scale, ws)
+    torch.cuda.synchronize()
+    _check_all(case, adm3, out3.cpu(), None, heads=[3, 40], what="build_work mask")
