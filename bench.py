@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--rank-of", type=int, default=0, metavar="G",
                     help="single GPU only: run the per-rank work of a G-GPU KV-head shard "
                          "(8/G heads, no collectives) -- what one rank of G does")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the step as one CUDA graph (auto: on when G > 1 or --rank-of, "
+                         "where a layer is short enough for host launch overhead to matter)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -143,11 +146,27 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(batch, layout, adm_mask, seconds, seed, layers):
+def host_cpu():
+    """(logical cores usable by this process, CPU model) of the host."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return int(cores or 1), model
+
+
+def cpu_baseline(batch, layout, adm_mask, seconds, seed, layers, threads=1):
     """Time the fp64 oracle (as it stands) on a bounded sample of the same workload:
     layer 0's attention for as many admitted slots x 64 Q heads as fit in ~`seconds`,
-    plus one literal Alg. 1 admission; extrapolated to one full step (x all slots, x layers)."""
+    plus one literal Alg. 1 admission; extrapolated to one full step (x all slots, x layers).
+    ``threads`` > 1: the oracle's independent (slot, head) pairs on that many host cores."""
     import oracle
+    threads = oracle.set_threads(threads)
     h = 8
     k, v = synth.make_kv(layout.num_pages, h, layout.page_size, 128, seed=seed)
     q = synth.make_q(batch.n_slot, 8 * h, 128, seed=seed)
@@ -177,13 +196,15 @@ def cpu_baseline(batch, layout, adm_mask, seconds, seed, layers):
     reqs = np.searchsorted(batch.req_slot_off, slots, side="right") - 1
     tok_all = int(batch.req_shared_len[reqs].astype(np.int64).sum() +
                   batch.slot_local_len[slots].astype(np.int64).sum())
+    oracle.set_threads(1)
     t_layer = t_att * tok_all / max(tok_done, 1)
     t_step = t_admit + layers * t_layer
-    return {"value": 1.0 / t_step, "unit": "steps/s", "cores": 1, "kind": "oracle",
-            "sample": f"layer 0: {done}/{len(slots)} admitted slots x 64 Q heads "
-                      f"({t_att:.1f} s, fp64 naive attention over materialised KV) + 1 literal "
-                      f"Alg. 1 admission ({t_admit * 1e3:.2f} ms); extrapolated by context tokens "
-                      f"to all slots and x{layers} layers",
+    return {"value": 1.0 / t_step, "unit": "steps/s", "cores": threads, "kind": "oracle",
+            "cpu_model": host_cpu()[1],
+            "sample": f"layer 0: {done}/{len(slots)} admitted slots x 64 Q heads on {threads} "
+                      f"thread(s) ({t_att:.1f} s, fp64 naive attention over materialised KV) + 1 "
+                      f"literal Alg. 1 admission ({t_admit * 1e3:.2f} ms); extrapolated by context "
+                      f"tokens to all slots and x{layers} layers",
             "admit_ms": t_admit * 1e3, "step_s_extrapolated": t_step}
 
 
@@ -218,7 +239,8 @@ def run_reference(args):
     per_step = max(1.0, 150.0 / max(1, args.steps + args.warmup))
     vals = []
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(batch, layout, adm, per_step, args.seed + i, args.layers)
+        cb = cpu_baseline(batch, layout, adm, per_step, args.seed + i, args.layers,
+                          threads=host_cpu()[0])
         if i >= args.warmup:
             vals.append(cb["step_s_extrapolated"])
     t_step = float(np.mean(vals))
@@ -229,7 +251,8 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOADS[args.config]}",
                        "policy": args.policy, "rho": RHO, "layers": args.layers},
-            "cpu_baseline": {"value": value, "unit": "steps/s", "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cb["cores"],
+                             "kind": "oracle", "cpu_model": cb["cpu_model"],
                              "sample": cb["sample"] + f"; mean over {args.steps} timed samples"},
             "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -312,22 +335,30 @@ def run_ours(args):
                  for _ in range(L)] if G > 1 else None)
     scale = 1.0 / math.sqrt(128)
     stream = torch.cuda.current_stream(dev)
+    comm = torch.cuda.Stream(dev) if G > 1 else None  # per-layer all-gathers ride here
     launches = [0]
 
     every = min(PROF_EVERY, L)
 
-    def step(prof=None, qs_=qs, outs_=outs, adm_ev=None):
+    def step(prof=None, qs_=qs, outs_=outs, adm_ev=None, gathered_=gathered):
+        """One decode step on the current stream.  G > 1: rank 0 alone runs the admission,
+        its admitted set is broadcast, the other ranks rebuild their work list from it
+        (taper_build_work); each layer's all-gather runs on a side stream, overlapped with
+        the next layer's attention, and the step joins it at the end."""
+        cur = torch.cuda.current_stream(dev)
         n = 0
         if adm_ev is not None:
-            adm_ev[0].record(stream)
-        T.taper_admit(db, MODEL, args.policy, RHO, adm, h, ws, 2, ctx=args.ctx)
-        n += T.taper_last_launch_count()
+            adm_ev[0].record(cur)
+        if rank == 0:
+            T.taper_admit(db, MODEL, args.policy, RHO, adm, h, ws, 2, ctx=args.ctx)
+            n += T.taper_last_launch_count()
         if G > 1:
             par.broadcast_admission(adm.slot_admitted)
-            T.taper_build_work(db, adm, h, ws)
-            n += T.taper_last_launch_count()
+            if rank != 0:
+                T.taper_build_work(db, adm, h, ws)
+                n += T.taper_last_launch_count()
         if adm_ev is not None:
-            adm_ev[1].record(stream)
+            adm_ev[1].record(cur)
         for l in range(L):
             sampled = prof is not None and l % every == every - 1
             if sampled:
@@ -337,7 +368,11 @@ def run_ours(args):
                 T.taper_set_profile_events(None)
             n += T.taper_last_launch_count()
             if G > 1:
-                par.gather_outputs(outs_[l], gathered[l])
+                comm.wait_stream(cur)
+                with torch.cuda.stream(comm):
+                    par.gather_outputs(outs_[l], gathered_[l])
+        if G > 1:
+            cur.wait_stream(comm)
         launches[0] = n
 
     def barrier():
@@ -352,6 +387,26 @@ def run_ours(args):
     if st != 0:
         raise RuntimeError(f"admission status {T.taper_status_string(st)}")
     adm_mask = adm.slot_admitted.cpu().numpy()[:S].copy()
+    use_graph = args.graph == "on" or (args.graph == "auto" and (G > 1 or args.rank_of > 0))
+    if backend != "nccl":
+        use_graph = False  # gloo collectives cannot be captured
+    graph = None
+    if use_graph:
+        # the whole step (admission, broadcast / work-list rebuild, 64 x attention,
+        # all-gathers) as one CUDA graph: PDL edges between the library's kernels are kept
+        graph = torch.cuda.CUDAGraph()
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(stream)
+        with torch.cuda.stream(gs):
+            step()  # warm the capture stream (NCCL communicators, allocator)
+        stream.wait_stream(gs)
+        torch.cuda.synchronize(dev)
+        with torch.cuda.graph(graph, stream=gs):
+            step()
+        n_graph_launches = launches[0]
+        for _ in range(2):
+            graph.replay()
+        barrier()
 
     # ---------------- timed region: K steps, CUDA events on the launching stream.
     # On every PROF_EVERY-th layer the library records 3 events (before / between / after
@@ -370,11 +425,22 @@ def run_ours(args):
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for i in range(args.steps):
-        step(prof[i], adm_ev=adm_evs[i])
+    if graph is None:
+        for i in range(args.steps):
+            step(prof[i], adm_ev=adm_evs[i])
+    else:
+        for i in range(args.steps):
+            graph.replay()
+        launches[0] = n_graph_launches
     ev1.record(stream)
     barrier()
     clocks = sampler.stop() if sampler else None
+    if graph is not None:
+        # kernel durations for the roofline: the same step run eagerly with the library's
+        # profile events (events cannot time nodes inside a replayed graph)
+        for i in range(args.steps):
+            step(prof[i], adm_ev=adm_evs[i])
+        barrier()
     elapsed = ev0.elapsed_time(ev1)
     t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
     if G > 1:
@@ -413,7 +479,11 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(batch, layout, adm_mask, args.cpu_seconds, args.seed, L)
+        # all host cores (the headline baseline) and one core, each ~cpu_seconds of work
+        cpu = cpu_baseline(batch, layout, adm_mask, args.cpu_seconds, args.seed, L,
+                           threads=host_cpu()[0])
+        one = cpu_baseline(batch, layout, adm_mask, args.cpu_seconds / 2, args.seed, L)
+        cpu["single_core"] = {k: one[k] for k in ("value", "unit", "cores", "sample")}
 
     if rank == 0:
         line = {
@@ -434,6 +504,9 @@ def run_ours(args):
                                 "no collectives; value = that rank's steps/s)"),
                 "l2": f"inputs larger than L2 ({layer_bytes / 1e9:.2f} GB K/V per layer per GPU)",
                 "step": f"admit + {L} x decode_attention (+ bcast/all-gather when G>1); no FFN",
+                "launch": ("one CUDA graph per step (kernel times from an eager profiled pass of "
+                           "the same step after the timed region)" if graph is not None else
+                           "eager launches; kernel times event-bracketed inside the timed region"),
             },
             "attn_gbs_per_gpu": attn_gbs, "step_hbm_gbs_total": step_gbs,
             "attn_frac_of_measured_hbm": attn_gbs / hbm_peak,
@@ -506,10 +579,12 @@ def run_e2e(args, T, torch, dist, G, batch, db, adm, ws, kvs, L, S, h, scale, de
                 dq[l].copy_(host_q[l], non_blocking=True)
                 q_ready[l].record(h2d)
         comp.wait_event(state_ready)
-        T.taper_admit(db, MODEL, args.policy, RHO, adm, h, ws, 2, ctx=args.ctx)
+        if rank == 0:
+            T.taper_admit(db, MODEL, args.policy, RHO, adm, h, ws, 2, ctx=args.ctx)
         if G > 1:
             par.broadcast_admission(adm.slot_admitted)
-            T.taper_build_work(db, adm, h, ws)
+            if rank != 0:
+                T.taper_build_work(db, adm, h, ws)
         for l in range(L):
             comp.wait_event(q_ready[l])
             T.taper_decode_attention(db, adm, kvs[l], dq[l], dout[l], None, scale, ws)

@@ -22,7 +22,10 @@
  *     TAPER_ERR_*).  Data errors that only the device can see are OR-ed into the device
  *     status word `taper_admission.status` (TAPER_STATUS_* bits); outputs are undefined
  *     when it is non-zero, and the caller reads it whenever it chooses.
- *   * Stateless and thread-safe: no globals except a thread-local last-error string.
+ *   * Stateless and thread-safe: no state survives a call except thread-local host
+ *     strings (last error, launch count) and the opt-in thread-local debug hooks
+ *     taper_set_profile_events / taper_set_trace_buffer (timing events and a pipeline
+ *     trace; they change what is recorded, never what is computed).
  *   * bf16 tensors are passed as void* to raw bf16 storage (no torch or CUDA types here).
  */
 #ifndef TAPER_H_
@@ -58,6 +61,13 @@ extern "C" {
                                           different cost, so the sort+scan is no longer
                                           guaranteed bit-identical to Alg. 1             */
 #define TAPER_STATUS_WORK_OVERFLOW 8   /* attention partials exceed the workspace        */
+#define TAPER_STATUS_WORK_MISMATCH 16  /* taper_decode_attention was given a workspace /
+                                          h_local other than the taper_admit or
+                                          taper_build_work call that wrote the work list:
+                                          nothing is computed, out is not written       */
+#define TAPER_STATUS_EMPTY_CONTEXT 32  /* an admitted slot has no context (Lsh_r + Lloc_s
+                                          = 0, [C-att-4]): softmax over an empty set; its
+                                          output rows are written as zeros, lse as -inf  */
 
 #define TAPER_MAX_SLOTS 4096   /* capacity of the single-CTA admission kernel (R and S)  */
 #define TAPER_HEAD_DIM 128     /* Qwen3-32B head_dim                     */
@@ -189,6 +199,18 @@ typedef struct {
 TAPER_API int taper_workspace_size(int32_t n_req, int32_t n_slot, int32_t h_local,
                          int64_t max_chunk_slots, size_t *bytes);
 
+/* The Eager bound of max_chunk_slots above, computed from HOST copies of the batch
+ * arrays (req_shared_len [R], req_slot_off [R+1], slot_local_len [S]; slot_seg_off /
+ * seg_len or NULL): every ready slot admitted, prefix chunks of
+ * taper_chunk_tokens(Lsh_r, h_local) tokens.  A bound for h_local = 1 holds for every
+ * h_local (the finest split).  Errors: TAPER_ERR_ARG (null array, non-monotone CSR,
+ * negative length).  [host]                                                            */
+TAPER_API int taper_max_chunk_slots(int32_t n_req, int32_t n_slot,
+                                    const int32_t *req_shared_len, const int32_t *req_slot_off,
+                                    const int32_t *slot_local_len, const int32_t *slot_seg_off,
+                                    const int32_t *seg_len, int32_t h_local,
+                                    int64_t *max_chunk_slots);
+
 /* One admission step (Sec. 3.3 + Alg. 1; fixed policies of App. D), then the attention
  * work list for this rank (h_local KV heads) is written into `workspace`.
  * Greedy with linear utility is evaluated as a sort of candidates by (dL, r, slot)
@@ -200,7 +222,10 @@ TAPER_API int taper_admit(const taper_batch *batch, const taper_latency_model *m
                 void *workspace, size_t workspace_bytes, void *stream);
 
 /* Rebuild adm_list / n_adm / req_width and the work list from slot_admitted alone (used
- * on every rank after rank 0's slot_admitted is broadcast, so ranks cannot diverge).    */
+ * on every rank after rank 0's slot_admitted is broadcast, so ranks cannot diverge).
+ * adm->status is overwritten with this call's data-error bits (the caller owns it for
+ * the step: a rank that only calls taper_build_work never keeps a stale bit).  diag is
+ * not written.                                                                          */
 TAPER_API int taper_build_work(const taper_batch *batch, const taper_admission *adm, int32_t h_local,
                      void *workspace, size_t workspace_bytes, void *stream);
 
@@ -211,8 +236,20 @@ TAPER_API int taper_build_work(const taper_batch *batch, const taper_admission *
  *   scale: softmax scale (1/sqrt(128))
  * Q head j of the rank's local KV head g is q[s, 8*g + j, :] (HF repeat_kv mapping).
  * The current token's K/V must already be in the cache (local segment, or the shared
- * segment of a serial request).  Rows of a page past a segment's end must hold finite
- * values (they are masked from the softmax but pass through the tensor cores).
+ * segment of a serial request).  Rows of a page past a segment's end may hold any bits
+ * (NaN included): their scores are masked and their V rows zeroed before the PV product.
+ * An admitted slot with an empty context writes zero rows (TAPER_STATUS_EMPTY_CONTEXT).
+ * Ordering contract (programmatic dependent launch): the kernels may start while the
+ * previous kernel on `stream` is still running.  They read the work list and the
+ * admission outputs only after that kernel's writes are visible (a device-side epoch
+ * that taper_admit / taper_build_work publishes is re-checked after the grid
+ * dependency), and q / the K/V pools only after the grid dependency.  The page tables
+ * (req_page_off ... seg_page_off) and the lengths in `batch` may be read early: they
+ * must be written before the taper_admit / taper_build_work call that produced the work
+ * list is enqueued (between that call and the attention calls only q and the K/V pool
+ * contents may change, e.g. by taper_append_kv or the QKV projection).  `workspace`
+ * and h_local must be the ones that call used (checked on the device:
+ * TAPER_STATUS_WORK_MISMATCH in adm->status).
  * Errors: TAPER_ERR_ARG, _CAPACITY, _CUDA.                                             */
 TAPER_API int taper_decode_attention(const taper_batch *batch, const taper_admission *adm,
                            const taper_kv *kv, const void *q, void *out, float *lse,
@@ -239,7 +276,8 @@ TAPER_API int taper_append_kv(const taper_batch *batch, const taper_admission *a
  * call's stream (cudaEvent_t handles passed as void*).  NULL disables.  [host]          */
 TAPER_API int taper_set_profile_events(void *const *events, int n_events);
 
-/* Debug hook: when non-NULL, attend_kernel records clock64() timestamps of its pipeline
+/* Debug hook (libraries built with -DTAPER_TRACE=1; the product build records nothing
+ * and ignores the buffer): when non-NULL, attend_kernel records clock64() timestamps of its pipeline
  * events (TMA issue, MMA issue/commit, softmax start/end, epilogue) for CTA 0 into
  * device_buffer[tile * 16 + event] (int64, capacity_tiles * 16 entries).  [host]        */
 TAPER_API int taper_set_trace_buffer(void *device_buffer, int capacity_tiles);

@@ -37,7 +37,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-                               "-shared", "-o", tmp, _SRC, "-lm"])
+                               "-fopenmp", "-shared", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -73,8 +73,17 @@ def _load():
         lib.oracle_attention_seg.restype = ctypes.c_int
         lib.oracle_attention_seg.argtypes = [i32, P, i32, i32, i32, i32, P, P, P, P, P, P, P, P,
                                              P, P, P, P, i32, P, P, f64, P, P]
+        lib.oracle_set_threads.restype = ctypes.c_int
+        lib.oracle_set_threads.argtypes = [ctypes.c_int]
+        lib.oracle_set_threads(1)  # serial unless a caller asks for the host cores
         _lib = lib
     return _lib
+
+
+def set_threads(n: int) -> int:
+    """Host threads for ``attention`` (independent (slot, head) pairs in parallel; each
+    pair's arithmetic is unchanged).  Returns the count in effect."""
+    return _load().oracle_set_threads(int(n))
 
 
 def _p(a: np.ndarray | None):

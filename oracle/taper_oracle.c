@@ -35,6 +35,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define ORACLE_OK 0
 #define ORACLE_STATUS_EMPTY_REQUEST 1 /* a request had no ready slot [C-adm-11] */
@@ -337,6 +340,17 @@ static double bf16_to_double(uint16_t h) {
  *   lse = log(sum_j exp(x_j))   (natural log)
  * q: [S][q_heads][d] bf16 bits.  out: [n_eval][d], lse: [n_eval].
  */
+static int attention_pair(int32_t e, int32_t R, const int32_t *off, int32_t h_kv,
+                          int32_t q_heads, int32_t d, int32_t page_size, int32_t group,
+                          const uint16_t *k_pages, const uint16_t *v_pages, const int32_t *Lsh,
+                          const int32_t *req_page_off, const int32_t *req_pages,
+                          const int32_t *Lloc, const int32_t *slot_page_off,
+                          const int32_t *slot_pages, const int32_t *slot_seg_off,
+                          const int32_t *seg_len, const int32_t *seg_page_off,
+                          const uint16_t *q, const int32_t *eval_slot,
+                          const int32_t *eval_qhead, double scale, double *out, double *lse);
+static inline int min_status(int a, int b) { return a < b ? a : b; }
+
 int oracle_attention_seg(int32_t R, const int32_t *off, int32_t h_kv, int32_t q_heads,
                          int32_t d, int32_t page_size, const uint16_t *k_pages,
                          const uint16_t *v_pages, const int32_t *Lsh,
@@ -348,7 +362,31 @@ int oracle_attention_seg(int32_t R, const int32_t *off, int32_t h_kv, int32_t q_
                          const int32_t *eval_qhead, double scale, double *out, double *lse) {
   if (h_kv <= 0 || q_heads % h_kv != 0 || d <= 0 || page_size <= 0) return ORACLE_ERR_ARG;
   int32_t group = q_heads / h_kv;
-  for (int32_t e = 0; e < n_eval; ++e) {
+  int status = ORACLE_OK;
+  /* The (slot, q-head) pairs are independent: with OpenMP (oracle_set_threads) they are
+   * spread over the host cores; each pair's arithmetic below is the same either way. */
+#pragma omp parallel for schedule(dynamic, 1) reduction(min : status)
+  for (int32_t e = 0; e < n_eval; ++e)
+    status = min_status(status, attention_pair(e, R, off, h_kv, q_heads, d, page_size, group,
+                                               k_pages, v_pages, Lsh, req_page_off, req_pages,
+                                               Lloc, slot_page_off, slot_pages, slot_seg_off,
+                                               seg_len, seg_page_off, q, eval_slot, eval_qhead,
+                                               scale, out, lse));
+  return status;
+}
+
+/* One (slot, q-head) pair of oracle_attention_seg. */
+static int attention_pair(int32_t e, int32_t R, const int32_t *off, int32_t h_kv,
+                          int32_t q_heads, int32_t d, int32_t page_size, int32_t group,
+                          const uint16_t *k_pages, const uint16_t *v_pages, const int32_t *Lsh,
+                          const int32_t *req_page_off, const int32_t *req_pages,
+                          const int32_t *Lloc, const int32_t *slot_page_off,
+                          const int32_t *slot_pages, const int32_t *slot_seg_off,
+                          const int32_t *seg_len, const int32_t *seg_page_off,
+                          const uint16_t *q, const int32_t *eval_slot,
+                          const int32_t *eval_qhead, double scale, double *out, double *lse) {
+  (void)h_kv;
+  {
     int32_t s = eval_slot[e];
     int32_t hq = eval_qhead[e];
     int32_t g = hq / group;
@@ -418,6 +456,17 @@ int oracle_attention_seg(int32_t R, const int32_t *off, int32_t h_kv, int32_t q_
     free(x);
   }
   return ORACLE_OK;
+}
+
+/* Host threads for oracle_attention(_seg) (1 = serial; the result does not depend on it). */
+int oracle_set_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n > 0 ? n : 1);
+  return n > 0 ? n : 1;
+#else
+  (void)n;
+  return 1;
+#endif
 }
 
 /* oracle_attention: oracle_attention_seg with one local segment per slot. */

@@ -536,8 +536,13 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     if (r < R && !(sh_status & TAPER_STATUS_BAD_LENGTH)) {
       int j = 0, base = w_loc[k];
       for (int s = p.off[r]; s < p.off[r + 1]; ++s) {
-        if (p.slot_admitted[s]) { p.adm_by_req[base + j] = s; p.slot_rank[s] = j; ++j; }
-        else p.slot_rank[s] = -2;
+        if (p.slot_admitted[s]) {
+          p.adm_by_req[base + j] = s; p.slot_rank[s] = j; ++j;
+          // softmax over an empty context is undefined [C-att-4]: flagged, zero output
+          if (p.Lsh[r] == 0 && p.Lloc[s] == 0) atomicOr(&sh_status, TAPER_STATUS_EMPTY_CONTEXT);
+        } else {
+          p.slot_rank[s] = -2;
+        }
       }
     }
   }
@@ -656,6 +661,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       for (int i = tid; i < D; i += blockDim.x) p.sorted[i] = p.items[i];
     }
   }
+  __syncthreads();  // every table above is written before the epoch below publishes it
   if (tid == 0) {
     int st = sh_status;
     int n_rc = tot_nc, n_rl = tot_nl;
@@ -670,8 +676,12 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     p.hdr[8] = 0;  // dynamic work counter of the next attend_kernel
     p.hdr[9] = 0;  // attend CTAs exited
     *p.n_adm = n_adm;
-    if (p.decide) *p.status = st;
-    else atomicOr(p.status, st);
+    *p.status = st;  // the caller owns the word for this step (admit and build_work alike)
+    // Work-list epoch: attend_kernel resolves its first item before its grid dependency
+    // resolves (PDL) and re-checks this epoch afterwards; the release orders every write
+    // of this kernel (the barrier above) before the new epoch becomes visible.
+    __threadfence();
+    st_release(p.hdr + kHdrEpoch, ld_acquire(p.hdr + kHdrEpoch) + 1);
   }
 }
 

@@ -41,6 +41,8 @@ extern "C" const char *taper_status_string(int code) {
     if (code & TAPER_STATUS_BAD_LENGTH) std::strcat(buf, "bad-length ");
     if (code & TAPER_STATUS_PRECISION) std::strcat(buf, "fp64-precision ");
     if (code & TAPER_STATUS_WORK_OVERFLOW) std::strcat(buf, "work-overflow ");
+    if (code & TAPER_STATUS_WORK_MISMATCH) std::strcat(buf, "work-mismatch ");
+    if (code & TAPER_STATUS_EMPTY_CONTEXT) std::strcat(buf, "empty-context ");
     return buf;
   }
   return "unknown error";
@@ -57,5 +59,40 @@ extern "C" int taper_workspace_size(int32_t n_req, int32_t n_slot, int32_t h_loc
   size_t part = size_t(max_chunk_slots) *
                 (size_t(h_local) * taper::kPartBytesPerCsHead + taper::kWorkBytesPerCs);
   *bytes = L.fixed + 1024 + part + 2048;
+  return TAPER_OK;
+}
+
+// Eager bound of the partial-row count (include/taper.h): per request, its ready branches x
+// prefix chunks, plus one local item per <= kLocalItemTiles tiles of each local segment.
+extern "C" int taper_max_chunk_slots(int32_t n_req, int32_t n_slot, const int32_t *lsh,
+                                     const int32_t *off, const int32_t *lloc,
+                                     const int32_t *seg_off, const int32_t *seg_len,
+                                     int32_t h_local, int64_t *out) {
+  if (!out || n_req < 0 || n_slot < 0 || h_local < 1 || h_local > 8 || !off ||
+      (n_req > 0 && !lsh) || (n_slot > 0 && !lloc) || (seg_off && !seg_len))
+    return taper::fail(TAPER_ERR_ARG, "bad taper_max_chunk_slots arguments");
+  if (off[0] != 0 || off[n_req] != n_slot)
+    return taper::fail(TAPER_ERR_ARG, "req_slot_off must run from 0 to n_slot");
+  constexpr int64_t per = int64_t(taper::kTileTokens) * taper::kLocalItemTiles;
+  int64_t total = 0;
+  for (int r = 0; r < n_req; ++r) {
+    if (off[r + 1] < off[r] || lsh[r] < 0)
+      return taper::fail(TAPER_ERR_ARG, "non-monotone req_slot_off or negative length");
+    const int64_t ck = taper_chunk_tokens(lsh[r], h_local);
+    total += int64_t(off[r + 1] - off[r]) * ((int64_t(lsh[r]) + ck - 1) / ck);
+  }
+  for (int s = 0; s < n_slot; ++s) {
+    if (!seg_off) {
+      if (lloc[s] < 0) return taper::fail(TAPER_ERR_ARG, "negative local length");
+      total += (int64_t(lloc[s]) + per - 1) / per;
+      continue;
+    }
+    if (seg_off[s + 1] < seg_off[s]) return taper::fail(TAPER_ERR_ARG, "non-monotone slot_seg_off");
+    for (int q = seg_off[s]; q < seg_off[s + 1]; ++q) {
+      if (seg_len[q] < 0) return taper::fail(TAPER_ERR_ARG, "negative segment length");
+      total += (int64_t(seg_len[q]) + per - 1) / per;
+    }
+  }
+  *out = total;
   return TAPER_OK;
 }

@@ -34,6 +34,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "host_common.h"
@@ -89,7 +90,11 @@ static_assert(kSmemBytes <= 232448, "exceeds 227 KB of dynamic SMEM per CTA");
 // epilogue; warp 10: V producer; warp 11: item scheduler (claims, resolves tiles, loads Q);
 // warps 12-15: softmax group 1.  A group owns 8-row blocks of the stacked rows.
 constexpr int kAttnThreads = 512;
-constexpr int kRingConsumers = 15;  // every warp but the scheduler releases each record
+// Every lane of the 15 consumer warps releases each record (and every scheduler lane
+// publishes it): each thread's own arrive orders its own SMEM accesses, which is also
+// the pattern compute-sanitizer's racecheck models (a lane-0 arrive after __syncwarp is
+// equally correct but reported as a hazard).
+constexpr int kRingConsumers = 15 * 32;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0;     // S^T 0 [0, 64), S^T 1 [64, 128): 64 tokens x N rows
 constexpr uint32_t kColO = 128;   // O^T 0 [128, 256), O^T 1 [256, 384): 128 d x 2N rows
@@ -107,14 +112,22 @@ struct AttnParams {
   float *part_lse, *part_o;
   int h_local, page_size;
   int tma5d;  // 1: page_size >= 64, one 5-D box per full tile; 0: 4-D boxes of one page
+  int cap_cs;  // partial capacity this call's workspace gives (checked against hdr[3])
   float scale_log2;
   long long *trace;  // debug: pipeline event timestamps of CTA 0 (taper_set_trace_buffer)
   int trace_cap;
 };
 
-// Debug trace: event e of tile/item index n -> trace[(n * 16 + e)] = clock64 (CTA 0 only).
+// Debug trace (builds with -DTAPER_TRACE=1 only; the product build compiles every probe
+// out -- their checks alone cost ~5 % of the softmax warps' issue slots, ncu r2a):
+// event e of tile/item index n -> trace[(n * 16 + e)] = clock64 (CTA 0 only).
+#ifndef TAPER_TRACE
+#define TAPER_TRACE 0
+#endif
+constexpr bool kTrace = TAPER_TRACE;
+__device__ __forceinline__ bool tracing(const AttnParams &p) { return kTrace && p.trace != nullptr; }
 __device__ __forceinline__ void trace_ev(const AttnParams &p, int e, uint32_t n) {
-  if (p.trace != nullptr && blockIdx.x == 0 && int(n) < p.trace_cap)
+  if (tracing(p) && blockIdx.x == 0 && int(n) < p.trace_cap)
     p.trace[(size_t)n * 16 + e] = clock64();
 }
 
@@ -148,12 +161,12 @@ struct TileInfo {
 __device__ __forceinline__ TileInfo tile_info(const AttnParams &p, const Item &x, int t) {
   TileInfo ti;
   if (!x.local) {
-    ti.pages = p.req_pages + __ldg(p.req_page_off + x.r);
+    ti.pages = p.req_pages + __ldcg(p.req_page_off + x.r);
     ti.tok0 = x.tb + t * kTile;
     ti.valid = min(kTile, x.te - ti.tok0);
   } else {
-    const int4 lt = __ldg(p.ltiles + x.tb + t);  // {slot, tok0, valid, segment or -1}
-    ti.pages = p.slot_pages + __ldg(p.slot_page_off + (lt.w >= 0 ? lt.w : lt.x));
+    const int4 lt = __ldcg(p.ltiles + x.tb + t);  // {slot, tok0, valid, segment or -1}
+    ti.pages = p.slot_pages + __ldcg(p.slot_page_off + (lt.w >= 0 ? lt.w : lt.x));
     ti.tok0 = lt.y;
     ti.valid = lt.z;
   }
@@ -561,8 +574,8 @@ __device__ __forceinline__ int ring_item(uint64_t *it_full, const ItemRec *recs,
   return *reinterpret_cast<const volatile int32_t *>(&recs[slot].it);
 }
 __device__ __forceinline__ void ring_release(uint64_t *it_empty, uint32_t k, int lane) {
-  __syncwarp();
-  if (lane == 0) mbar_arrive(it_empty + (k % kItemRing));
+  (void)lane;
+  mbar_arrive(it_empty + (k % kItemRing));
 }
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
@@ -597,7 +610,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int h = p.h_local;
-  if (p.trace != nullptr && tid == 0) {  // per-CTA wall-clock span (debug trace)
+  if (tracing(p) && tid == 0) {  // per-CTA wall-clock span (debug trace)
     unsigned long long g;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
     p.trace[(size_t)(3000 + blockIdx.x) * 16 + 0] = (long long)g;
@@ -628,7 +641,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_init(ml_full + i, 256);
     }
     for (int i = 0; i < kItemRing; ++i) {
-      mbar_init(it_full + i, 1);
+      mbar_init(it_full + i, 32);
       mbar_init(it_empty + i, kRingConsumers);
     }
     mbar_init(sched_go, 1);
@@ -643,11 +656,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // PDL: the prologue above overlapped the previous kernel; the merge kernel may launch now
-  // (it waits for per-request completion counters); wait for the previous kernel's memory.
-  pdl_launch_dependents();
-  // The scheduler warp claims and resolves its first item before waiting (see below).
-  if (!(kEarlyClaim && warp == 11)) pdl_wait();
+  // PDL: the prologue above overlapped the previous kernel; wait for its memory, then let
+  // the merge kernel launch (it reads the work list, which is complete and visible once
+  // this grid's dependency has resolved; its warps then wait for per-request completion
+  // counters).  The scheduler warp resolves its first item before waiting (see below).
+  if (!(kEarlyClaim && warp == 11)) {
+    pdl_wait();
+    pdl_launch_dependents();
+  }
 
   if (warp == 11) {
     // ======================= item scheduler ==================================================
@@ -657,26 +673,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // Q^T (one 2 KB TMA box per branch: its 8 GQA rows, SW128) into Q buffer k & 1.  The
     // dependent global loads of an item thus overlap the previous item.
     const int box_tok = p.page_size < kTile ? p.page_size : kTile;
-    const int n_desc = __ldg(p.hdr) + __ldg(p.hdr + 5);
-    const int n_items = n_desc * h;
+    // Work-list epoch (hdr[10]), read with acquire BEFORE any table: if it is the epoch of
+    // the admission that wrote the tables, those tables are visible; if that admission is
+    // the kernel still draining in front of this one, the epoch moves before the re-check
+    // below and the first item is resolved again (include/taper.h ordering contract).
+    int epoch = kEarlyClaim ? ld_acquire(p.hdr + kHdrEpoch) : 0;
+    // items per KV head, or none if the work list was written for another workspace / h
+    auto count_items = [&]() {
+      const bool ok = __ldcg(p.hdr + 4) == h && __ldcg(p.hdr + 3) == p.cap_cs;
+      return ok ? (__ldcg(p.hdr) + __ldcg(p.hdr + 5)) * h : 0;
+    };
+    int n_items = count_items();
     int *work_counter = p.hdr + 8;
-    for (uint32_t k = 0;; ++k) {
-      if (k >= 1) mbar_wait(sched_go, (k - 1) & 1);  // K producer started item k-1
-      int it = 0;
-      // first item: claim index blockIdx.x (static), later ones from the counter
-      if (lane == 0)
-        it = (kEarlyClaim && k == 0) ? int(blockIdx.x)
-                                     : (kEarlyClaim ? int(gridDim.x) : 0) + atomicAdd(work_counter, 1);
-      it = __shfl_sync(0xffffffffu, it, 0);
-      if (it >= n_items) it = -1;
-      const uint32_t slot = k % kItemRing;
-      ItemRec *rec = recs + slot;
-      mbar_wait(it_empty + slot, ((k / kItemRing) & 1) ^ 1);
-      int w = 0, adm_off = 0, g = 0;
+    // claim index `it` -> the SMEM record (descriptor, per-tile geometry and pages)
+    auto resolve = [&](ItemRec *rec, int it, int &w, int &adm_off, int &g) {
+      w = 0; adm_off = 0; g = 0;
       if (it >= 0) {
         const int qi = it / h;  // claim index -> descriptor (longest first), then KV head
         g = it - qi * h;
-        const int32_t d = lane < 8 ? __ldg(reinterpret_cast<const int32_t *>(p.sorted + qi) + lane) : 0;
+        const int32_t d = lane < 8 ? __ldcg(reinterpret_cast<const int32_t *>(p.sorted + qi) + lane) : 0;
         const int nt = __shfl_sync(0xffffffffu, d, 6);
         Item x;
         x.r = __shfl_sync(0xffffffffu, d, 0);
@@ -693,17 +708,40 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
           for (int b = 0; b < kTile / 16; ++b)
             rec->pg[t][b] =
-                b * box_tok < ti.valid ? __ldg(ti.pages + (ti.tok0 + b * box_tok) / p.page_size) : 0;
+                b * box_tok < ti.valid ? __ldcg(ti.pages + (ti.tok0 + b * box_tok) / p.page_size) : 0;
         }
       }
       if (lane == 0) { rec->it = it; rec->g = g; }
+    };
+    for (uint32_t k = 0;; ++k) {
+      if (k >= 1) mbar_wait(sched_go, (k - 1) & 1);  // K producer started item k-1
+      int it = 0;
+      // first item: claim index blockIdx.x (static), later ones from the counter
+      if (lane == 0)
+        it = (kEarlyClaim && k == 0) ? int(blockIdx.x)
+                                     : (kEarlyClaim ? int(gridDim.x) : 0) + atomicAdd(work_counter, 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      const uint32_t slot = k % kItemRing;
+      ItemRec *rec = recs + slot;
+      mbar_wait(it_empty + slot, ((k / kItemRing) & 1) ^ 1);
+      int w, adm_off, g;
+      for (bool early = kEarlyClaim && k == 0;;) {
+        resolve(rec, it < n_items ? it : -1, w, adm_off, g);
+        if (!early) break;
+        // The first record was resolved while the previous kernel drained.  Now wait for
+        // it (q, the K/V pools and a just-written work list become visible), let the merge
+        // kernel launch, and re-resolve if an admission published a new work list meanwhile.
+        early = false;
+        pdl_wait();
+        pdl_launch_dependents();
+        if (ld_acquire(p.hdr + kHdrEpoch) == epoch) break;
+        n_items = count_items();
+        __syncwarp();
+      }
+      if (it >= n_items) it = -1;
       __syncwarp();
-      if (lane == 0) mbar_arrive(it_full + slot);  // release: the record is visible
+      mbar_arrive(it_full + slot);  // release (every lane): the record is visible
       if (it < 0) break;
-      // Early claim: the first record (descriptor, tiles, pages -- tables written by
-      // taper_admit or the caller before the previous kernel started) was resolved while the
-      // previous kernel finished; q may come from the kernel just before, so wait here.
-      if (kEarlyClaim && k == 0) pdl_wait();
       // Q^T of the item's w branches: box {64 d, 8 rows, 2 d-halves} of q viewed as
       // (d-lo, GQA row, d-half, slot * h + g) -> [d-half][8 rows][128 B] per branch
       const uint32_t qb = k & 1;
@@ -753,7 +791,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint8_t *dst = ring + st * kStageBytes;
         mbar_wait(ring_empty + st, ((n_prod / n_stages) & 1) ^ 1);
         if (is_k && lane == 0) trace_ev(p, 0, n_prod);
-        if (is_k && lane == 0 && p.trace != nullptr && t == 0 && n_prod == 0) {
+        if (is_k && lane == 0 && tracing(p) && t == 0 && n_prod == 0) {
           unsigned long long g;
           asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
           p.trace[(size_t)(3000 + blockIdx.x) * 16 + 2] = (long long)g;  // first TMA issued
@@ -805,7 +843,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       decode_item(recs + item_idx % kItemRing, x);
       ring_release(it_empty, item_idx, lane);
 #ifdef TAPER_TRACE_ITEMS
-      if (it < 0 && lane == 0 && p.trace != nullptr) {  // per-CTA items and tiles (debug)
+      if (it < 0 && lane == 0 && tracing(p)) {  // per-CTA items and tiles (debug)
         p.trace[(size_t)(3000 + blockIdx.x) * 16 + 3] = item_idx;
         p.trace[(size_t)(3000 + blockIdx.x) * 16 + 4] = n;
       }
@@ -930,7 +968,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_wait(ml_full + ob, (item_idx >> 1) & 1);
       mbar_wait(o_full + ob, (item_idx >> 1) & 1);
       if (warp == 6 && lane == 0) trace_ev(p, 10, 2048 + item_idx);
-      if (p.trace != nullptr && blockIdx.x == 0 && warp == 6 && lane == 0 &&
+      if (tracing(p) && blockIdx.x == 0 && warp == 6 && lane == 0 &&
           2048 + int(item_idx) < p.trace_cap) {
         long long *tr = p.trace + (size_t)(2048 + item_idx) * 16;
         tr[13] = x.w; tr[14] = x.nt; tr[15] = x.local;
@@ -982,7 +1020,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       p.hdr[9] = 0;
     }
   }
-  if (p.trace != nullptr && tid == 0) {
+  if (tracing(p) && tid == 0) {
     unsigned long long g;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
     p.trace[(size_t)(3000 + blockIdx.x) * 16 + 1] = (long long)g;
@@ -1003,6 +1041,8 @@ struct MergeParams {
   __nv_bfloat16 *out;
   float *lse_out;
   int h_local;
+  int cap_cs;       // partial capacity of this call's workspace (checked against hdr[3])
+  int32_t *status;  // taper_admission.status (TAPER_STATUS_WORK_MISMATCH)
 };
 
 // Per (admitted slot, KV head): the slot's partials are 8 contiguous GQA rows (4 KB) per
@@ -1014,7 +1054,7 @@ struct MergeParams {
 // completion counter), so the merge overlaps the attend kernel's tail.
 __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool tr = p.trace != nullptr && threadIdx.x == 0 && 3200 + int(blockIdx.x) < p.trace_cap;
+  const bool tr = kTrace && p.trace != nullptr && threadIdx.x == 0 && 3200 + int(blockIdx.x) < p.trace_cap;
   if (tr) {
     unsigned long long g;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
@@ -1022,13 +1062,18 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) 
   }
   pdl_launch_dependents();
   const int h = p.h_local;
-  const int n_adm = __ldg(p.hdr + 2);
+  // the work list is visible: attend_kernel triggers this launch only after its own grid
+  // dependency (the admission) resolved.  A work list written for another workspace or
+  // h_local computes nothing (attend_kernel claims no items either).
+  const bool match = __ldcg(p.hdr + 4) == h && __ldcg(p.hdr + 3) == p.cap_cs;
+  if (!match && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(p.status, TAPER_STATUS_WORK_MISMATCH);
+  const int n_adm = match ? __ldcg(p.hdr + 2) : 0;
   const int qheads = kGroup * h;
   for (int k = blockIdx.x; k < n_adm; k += gridDim.x) {
     // {slot, first shared partial, prefix chunks, width}, {first local partial, local items,
     // request, items of the request per KV head}
-    const int4 md = __ldg(p.merge_desc + 2 * k);
-    const int4 ml = __ldg(p.merge_desc + 2 * k + 1);
+    const int4 md = __ldcg(p.merge_desc + 2 * k);
+    const int4 ml = __ldcg(p.merge_desc + 2 * k + 1);
     const int s = md.x, nc = md.z, w = md.w, r = ml.z;
     const int nq = nc + ml.y, target = ml.w;
     for (int g = warp; g < h; g += kMergeThreads / 32) {
@@ -1078,7 +1123,7 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) 
       }
 #pragma unroll
       for (int a = 0; a < kGroup; ++a) {
-        const float inv = 1.f / Z[a];
+        const float inv = Z[a] > 0.f ? 1.f / Z[a] : 0.f;  // empty context: zeros, lse -inf
         __align__(8) __nv_bfloat162 o2[2];
         o2[0] = __floats2bfloat162_rn(acc[a].x * inv, acc[a].y * inv);
         o2[1] = __floats2bfloat162_rn(acc[a].z * inv, acc[a].w * inv);
@@ -1238,14 +1283,20 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   if (rc == TAPER_OK) rc = make_q_map(&tmQ, q, S, kv->h_local);
   if (rc != TAPER_OK) return rc;
 
-  static thread_local bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kSmemBytes);
-    if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(attend_kernel)");
-    attr_set = true;
+  {  // the SMEM opt-in is a per-device function attribute
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (!(attr_set.load(std::memory_order_relaxed) & bit)) {
+      cudaError_t e = cudaFuncSetAttribute(attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kSmemBytes);
+      if (e != cudaSuccess) return fail_cuda(e, "cudaFuncSetAttribute(attend_kernel)");
+      attr_set.fetch_or(bit);
+    }
   }
   WsTables tabs = ws_tables(workspace_bytes, R, S, h);
+  if (!adm->status) return fail(TAPER_ERR_ARG, "null admission status");
   AttnParams ap;
   ap.slot_page_off = batch->slot_seg_off ? kv->seg_page_off : kv->slot_page_off;
   ap.slot_pages = kv->slot_pages;
@@ -1261,6 +1312,7 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   ap.h_local = h;
   ap.page_size = kv->page_size;
   ap.tma5d = kv->page_size >= kTile ? 1 : 0;
+  ap.cap_cs = int(tabs.cap_cs > 0x7fffffff ? 0x7fffffff : tabs.cap_cs);  // as admit stores it
   ap.scale_log2 = scale * 1.4426950408889634f;
   ap.trace = g_trace;
   ap.trace_cap = g_trace_cap;
@@ -1295,6 +1347,8 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   mp.out = static_cast<__nv_bfloat16 *>(out);
   mp.lse_out = lse;
   mp.h_local = h;
+  mp.cap_cs = ap.cap_cs;
+  mp.status = adm->status;
   const int grid = S > 0 ? S : 1;  // CTAs beyond the admitted count exit at once
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kMergeThreads);

@@ -37,10 +37,20 @@ def q_head_range(rank: int, world: int) -> tuple[int, int]:
     return GQA * g0, GQA * g1
 
 
+def _host_staged(group) -> bool:
+    """gloo (CPU tests, the one-GPU multi-rank checks) exchanges host tensors."""
+    return dist.get_backend(group) == "gloo"
+
+
 def broadcast_admission(slot_admitted: torch.Tensor, group=None) -> torch.Tensor:
     """Replace every rank's admitted-slot mask by rank 0's (in place)."""
     if dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.broadcast(slot_admitted, src=0, group=group)
+        if slot_admitted.is_cuda and _host_staged(group):
+            h = slot_admitted.cpu()
+            dist.broadcast(h, src=0, group=group)
+            slot_admitted.copy_(h)
+        else:
+            dist.broadcast(slot_admitted, src=0, group=group)
     return slot_admitted
 
 
@@ -52,6 +62,13 @@ def gather_outputs(out_local: torch.Tensor, gathered: torch.Tensor | None = None
         return out_local.unsqueeze(0)
     if gathered is None:
         gathered = out_local.new_empty((world,) + tuple(out_local.shape))
+    if out_local.is_cuda and _host_staged(group):
+        # bit patterns as int16 (gloo reduces no bf16 here; a gather only moves bits)
+        hg = torch.empty(gathered.shape, dtype=torch.int16)
+        dist.all_gather_into_tensor(hg.view(-1, *out_local.shape[1:]),
+                                    out_local.cpu().view(torch.int16), group=group)
+        gathered.copy_(hg.view(gathered.dtype))
+        return gathered
     # concatenated [G*S, ...] view: the form both NCCL and gloo accept
     dist.all_gather_into_tensor(gathered.view(-1, *out_local.shape[1:]), out_local.contiguous(),
                                 group=group)

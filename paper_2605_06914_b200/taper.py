@@ -21,9 +21,10 @@ TAPER_POLICY_OFF, TAPER_POLICY_CAP, TAPER_POLICY_EAGER, TAPER_POLICY_GREEDY = 0,
 POLICY = {"off": 0, "cap": 1, "eager": 2, "taper": 3, "greedy": 3}
 TAPER_STATUS_EMPTY_REQUEST, TAPER_STATUS_BAD_LENGTH = 1, 2
 TAPER_STATUS_PRECISION, TAPER_STATUS_WORK_OVERFLOW = 4, 8
+TAPER_STATUS_WORK_MISMATCH, TAPER_STATUS_EMPTY_CONTEXT = 16, 32
 TAPER_MAX_SLOTS = 4096
 TAPER_CHUNK_TOKENS = 4096
-EXPORTS = ("taper_workspace_size", "taper_admit", "taper_build_work", "taper_decode_attention",
+EXPORTS = ("taper_workspace_size", "taper_max_chunk_slots", "taper_admit", "taper_build_work", "taper_decode_attention",
            "taper_append_kv",
            "taper_status_string", "taper_last_error", "taper_last_launch_count",
            "taper_set_profile_events", "taper_set_trace_buffer")
@@ -70,6 +71,9 @@ def load_library() -> ctypes.CDLL:
     P = ctypes.POINTER
     lib.taper_workspace_size.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                          ctypes.c_int64, P(ctypes.c_size_t)]
+    lib.taper_max_chunk_slots.argtypes = [ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp,
+                                          ctypes.c_int32, P(ctypes.c_int64)]
+    lib.taper_max_chunk_slots.restype = ctypes.c_int
     lib.taper_admit.argtypes = [P(_Batch), P(_Model), P(_Policy), P(_Admission), ctypes.c_int32,
                                 _vp, ctypes.c_size_t, _vp]
     lib.taper_build_work.argtypes = [P(_Batch), P(_Admission), ctypes.c_int32, _vp,
@@ -219,35 +223,27 @@ def page_tables_to_device(layout, device="cuda"):
             t(pad(layout.slot_pages)))
 
 
-TAPER_TILE_TOKENS = 64
-TAPER_LOCAL_ITEM_TILES = 16
-
-
-def chunk_tokens(lsh, h_local: int):
-    """taper_chunk_tokens(Lsh, h_local) of include/taper.h (vectorised): the shared-prefix
-    split clamp(roundup_64(max(512 h, Lsh / 8)), 1024, 4096) -- sizing only."""
-    c = np.maximum(512 * h_local, np.asarray(lsh, np.int64) // 8)
-    c = (c + 63) // 64 * 64
-    return np.clip(c, 1024, TAPER_CHUNK_TOKENS)
-
-
 def max_chunk_slots(req_shared_len, req_slot_off, slot_local_len, seg_len=None,
-                    h_local: int = 1) -> int:
-    """Eager-case partial-row count for taper_workspace_size: per request, its ready
-    branches x prefix chunks of TAPER_CHUNK_TOKENS tokens, plus one local item per <= 16
-    64-token tiles of each branch's own segment (or of each local segment, if given;
-    include/taper.h)."""
-    lsh = np.asarray(req_shared_len, np.int64)
-    off = np.asarray(req_slot_off, np.int64)
-    lloc = np.asarray(slot_local_len, np.int64)
-    n = off[1:] - off[:-1]
-    ck = chunk_tokens(lsh, h_local)  # default h_local = 1: the finest split (always enough)
-    chunks = (lsh + ck - 1) // ck
-    per_item = TAPER_TILE_TOKENS * TAPER_LOCAL_ITEM_TILES
+                    h_local: int = 1, slot_seg_off=None) -> int:
+    """taper_max_chunk_slots (include/taper.h): the Eager bound of the partial rows for
+    taper_workspace_size, from host arrays.  ``seg_len`` without ``slot_seg_off``: the
+    segments are counted flat (the bound only needs their lengths)."""
+    a = lambda x: np.ascontiguousarray(np.asarray(x, np.int32))
+    lsh, off, lloc = a(req_shared_len), a(req_slot_off), a(slot_local_len)
+    R, S = len(lsh), len(lloc)
+    so = sl = None
     if seg_len is not None:
-        lloc = np.asarray(seg_len, np.int64)
-    local_items = (lloc + per_item - 1) // per_item
-    return int((n * chunks).sum() + local_items.sum())
+        sl = a(seg_len) if len(seg_len) else np.zeros(1, np.int32)
+        so = a(slot_seg_off) if slot_seg_off is not None else None
+        if so is None:  # lengths only: one pseudo-slot per segment, zero-length slots
+            so = np.zeros(S + 1, np.int32)
+            so[S] = len(seg_len)
+    out = ctypes.c_int64(0)
+    ptr = lambda x: None if x is None else x.ctypes.data_as(ctypes.c_void_p)
+    _check(_lib.taper_max_chunk_slots(R, S, ptr(lsh), ptr(off), ptr(lloc if so is None else np.zeros(max(S, 1), np.int32)),
+                                      ptr(so), ptr(sl), h_local, ctypes.byref(out)),
+           "taper_max_chunk_slots")
+    return out.value
 
 
 # ------------------------------------------------------------------ C-ABI calls

@@ -9,6 +9,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
+import scripts._tracelib  # noqa: E402,F401  (TAPER_TRACE build)
 from paper_2605_06914_b200 import taper as T  # noqa: E402
 
 

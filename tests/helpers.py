@@ -15,12 +15,20 @@ TOL_ABS, TOL_REL = 2e-3, 1e-2  # BASELINE.json north_star; allclose reading [C-a
 
 class Case:
     def __init__(self, batch, page=64, h_kv=8, seed=0, variant="flat", local_capacity=None,
-                 layout_seed=1):
+                 layout_seed=1, device_kv=False):
         self.batch = batch
         self.h_kv = h_kv
         self.layout = synth.make_layout(batch, page, np.random.default_rng(layout_seed),
                                         spare_pages=1, local_capacity=local_capacity)
-        self.k, self.v = synth.make_kv(self.layout.num_pages, h_kv, page, 128, seed)
+        # device_kv: draw the pools on the GPU (full-size configs: tens of GB of bf16) and
+        # keep a host copy for the oracle; the GPU run then uses the device pools as drawn
+        self.kv_dev = None
+        if device_kv:
+            kd, vd = synth.make_kv(self.layout.num_pages, h_kv, page, 128, seed, device="cuda")
+            self.kv_dev = (kd, vd)
+            self.k, self.v = kd.cpu(), vd.cpu()
+        else:
+            self.k, self.v = synth.make_kv(self.layout.num_pages, h_kv, page, 128, seed)
         gain = 4.0 if variant == "peaked" else 1.0
         self.q = synth.make_q(batch.n_slot, 8 * h_kv, 128, seed, gain)
         if variant == "sink":
@@ -46,8 +54,11 @@ class Case:
         spg = None
         if self.layout.seg_page_off is not None:
             spg = torch.as_tensor(np.concatenate([self.layout.seg_page_off, [0]]).astype(np.int32)).to(dev)
-        kv = T.DeviceKV(self.k[:, g0:g1].contiguous().to(dev), self.v[:, g0:g1].contiguous().to(dev),
-                        rpo, rp, spo, sp, spg)
+        if self.kv_dev is not None and (g0, g1) == (0, self.h_kv):
+            kd, vd = self.kv_dev
+        else:
+            kd, vd = self.k[:, g0:g1].contiguous().to(dev), self.v[:, g0:g1].contiguous().to(dev)
+        kv = T.DeviceKV(kd, vd, rpo, rp, spo, sp, spg)
         q = self.q[:, 8 * g0:8 * g1].contiguous().to(dev)
         out = torch.full_like(q, float("nan"))
         lse = torch.full((b.n_slot, 8 * h), float("nan"), device=dev) if with_lse else None

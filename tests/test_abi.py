@@ -44,8 +44,15 @@ def test_host_validation_without_gpu():
     # branch with local tokens (65, 1, 2, 3 -> 4 items of <= 16 x 64 tokens)
     assert T.max_chunk_slots([4097, 1, 0], [0, 3, 4, 6], [0, 65, 1, 0, 2, 3], h_local=8) == 6 + 1 + 0 + 4
     # taper_chunk_tokens(Lsh, h) (include/taper.h): 4k prefix -> 1024 at h <= 2, 2048 at
-    # h = 4, 4096 at h = 8; a 24k prefix keeps 3072-token chunks at any h < 8
-    assert [int(T.chunk_tokens(4096, h)) for h in (1, 2, 4, 8)] == [1024, 1024, 2048, 4096]
-    assert [int(T.chunk_tokens(24576, h)) for h in (1, 4, 8)] == [3072, 3072, 4096]
-    assert int(T.chunk_tokens(100, 8)) == 4096 and int(T.chunk_tokens(100, 1)) == 1024
+    # h = 4, 4096 at h = 8; a 24k prefix keeps 3072-token chunks at any h < 8 (probed as the
+    # chunk count of a one-slot request)
+    chunks = lambda lsh, h: T.max_chunk_slots([lsh], [0, 1], [0], h_local=h)
+    assert [chunks(4096, h) for h in (1, 2, 4, 8)] == [4, 4, 2, 1]
+    assert [chunks(24576, h) for h in (1, 4, 8)] == [8, 8, 6]
+    assert chunks(100, 8) == 1 and chunks(1025, 1) == 2 and chunks(0, 1) == 0
+    # local segments count per segment; bad CSR is an argument error
+    assert T.max_chunk_slots([0], [0, 1], [1030], [1024, 6], h_local=8,
+                             slot_seg_off=[0, 2]) == 2
+    with pytest.raises(T.TaperError):
+        T.max_chunk_slots([5], [0, 2], [1], h_local=8)
     assert T.max_chunk_slots([4097, 1, 0], [0, 3, 4, 6], [0, 65, 1, 0, 2, 3]) == 15 + 1 + 0 + 4

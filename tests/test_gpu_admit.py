@@ -37,7 +37,11 @@ def _compare(b, model, policy, rho, cap=2, ctx="per_sequence", utility=None):
     assert n_adm == int(o.slot_admitted.sum())
     np.testing.assert_array_equal(g.adm_list.cpu().numpy()[:n_adm], np.flatnonzero(o.slot_admitted))
     st = int(g.status.item())
-    assert (st & 1) == (o.status & 1) and (st & ~(1 | 4)) == 0, st
+    assert (st & 1) == (o.status & 1) and (st & ~(1 | 4 | 32)) == 0, st
+    # TAPER_STATUS_EMPTY_CONTEXT iff some admitted slot has Lsh_r + Lloc_s = 0 [C-att-4]
+    req = np.searchsorted(b.req_slot_off, np.arange(S), side="right") - 1
+    empty = (o.slot_admitted.astype(bool) & (b.req_shared_len[req] == 0) & (b.slot_local_len == 0)).any()
+    assert bool(st & 32) == bool(empty), st
     return o
 
 

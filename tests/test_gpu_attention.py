@@ -39,7 +39,7 @@ def test_c1_tiny_all_widths(w1):
 
 
 @pytest.mark.parametrize("variant", ["flat", "peaked", "sink"])
-@pytest.mark.parametrize("page", [16, 64, 128])
+@pytest.mark.parametrize("page", [16, 32, 64, 128])
 def test_multi_chunk_ragged(variant, page):
     # prefixes spanning several 4096-token chunks with ragged tails, up to 16 branches
     # (128 stacked rows), serial requests, local lengths crossing page boundaries
@@ -135,7 +135,7 @@ def test_partial_admission_outputs(policy):
     _check_all(case, adm, out, lse, heads=[0, 9, 63], what=policy)
 
 
-@pytest.mark.parametrize("page", [16, 64])
+@pytest.mark.parametrize("page", [16, 32, 64])
 def test_garbage_past_sequence_end(page):
     """Token slots of the pool past every segment's end (the tail of its last page, spare
     pages) hold NaN: a partial tile must never let them reach O (P = 0 there, but
@@ -320,6 +320,27 @@ def test_full_size_one_rank_of_8_sampled(name):
     es, eh = np.repeat(slots, 8), np.tile(np.arange(8), len(slots))
     ref, ref_lse = case.run_oracle(es, eh)
     assert_close(out[es, eh].float().numpy(), ref, f"{name} rank of 8")
+    np.testing.assert_allclose(lse[es, eh].numpy(), ref_lse, atol=2e-3, rtol=1e-4)
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_full_size_h8_sampled(name):
+    """BASELINE.json configs[2] / [4] at full size with all 8 KV heads on one GPU -- the launch
+    configuration `bench.py --config c3 | c5` times (c3: 8-16 branches on 16-32k prefixes;
+    c5: 256 requests, 1k-32k prefixes, ~11 GB of K/V): sampled admitted slots x 4 Q heads
+    (one per pair of KV heads) against the oracle, every admitted slot finite."""
+    b = synth.config_batch(name, seed=2)
+    case = Case(b, h_kv=8, seed=2, device_kv=True)
+    adm, out, lse = case.run_gpu(policy="eager")
+    mask = adm.slot_admitted.cpu().numpy()[:b.n_slot]
+    assert mask.all()
+    assert torch.isfinite(out.float()).all()
+    rng = np.random.default_rng(2)
+    slots = np.sort(rng.choice(b.n_slot, 40, replace=False))
+    heads = np.array([3, 20, 41, 62])
+    es, eh = np.repeat(slots, len(heads)), np.tile(heads, len(slots))
+    ref, ref_lse = case.run_oracle(es, eh)
+    assert_close(out[es, eh].float().numpy(), ref, f"{name} h=8")
     np.testing.assert_allclose(lse[es, eh].numpy(), ref_lse, atol=2e-3, rtol=1e-4)
 
 

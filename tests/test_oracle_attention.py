@@ -260,3 +260,23 @@ def test_segments_must_sum_to_local_length():
     b.seg_len[0] += 1
     with pytest.raises(ValueError):
         _run_seg(b, lay, k, v, q, np.array([0]), np.array([0]))
+
+
+def test_threads_do_not_change_bits():
+    """oracle.set_threads only spreads independent (slot, head) pairs over host cores: the
+    results are bit-identical to the serial evaluation."""
+    b = synth.config_batch("c1", seed=3)
+    lay = synth.make_layout(b, 16, np.random.default_rng(2), spare_pages=1)
+    k, v = synth.make_kv(lay.num_pages, 8, 16, 128, seed=3)
+    q = synth.make_q(b.n_slot, 64, 128, seed=3)
+    es, eh = np.meshgrid(np.arange(b.n_slot), np.arange(0, 64, 5), indexing="ij")
+    args = (b.req_slot_off, b.req_shared_len, b.slot_local_len, lay.req_page_off, lay.req_pages,
+            lay.slot_page_off, lay.slot_pages, k, v, q, es.ravel(), eh.ravel())
+    oracle.set_threads(1)
+    o1, l1 = oracle.attention(*args)
+    try:
+        oracle.set_threads(4)
+        o4, l4 = oracle.attention(*args)
+    finally:
+        oracle.set_threads(1)
+    assert o1.tobytes() == o4.tobytes() and l1.tobytes() == l4.tobytes()
