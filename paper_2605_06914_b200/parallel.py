@@ -63,10 +63,11 @@ def gather_outputs(out_local: torch.Tensor, gathered: torch.Tensor | None = None
     if gathered is None:
         gathered = out_local.new_empty((world,) + tuple(out_local.shape))
     if out_local.is_cuda and _host_staged(group):
-        # bit patterns as int16 (gloo reduces no bf16 here; a gather only moves bits)
-        hg = torch.empty(gathered.shape, dtype=torch.int16)
-        dist.all_gather_into_tensor(hg.view(-1, *out_local.shape[1:]),
-                                    out_local.cpu().view(torch.int16), group=group)
+        # bit patterns as bytes (gloo's all-gather takes neither bf16 nor int16 here; a
+        # gather only moves bits)
+        hg = torch.empty(gathered.shape, dtype=gathered.dtype).view(torch.uint8)
+        dist.all_gather_into_tensor(hg.view(-1, *hg.shape[2:]),
+                                    out_local.cpu().contiguous().view(torch.uint8), group=group)
         gathered.copy_(hg.view(gathered.dtype))
         return gathered
     # concatenated [G*S, ...] view: the form both NCCL and gloo accept
