@@ -29,7 +29,12 @@ constexpr int kItemCost0 = TAPER_ITEM_COST0;  // fixed per-item cost in the clai
 #ifndef TAPER_NARROW_COST
 #define TAPER_NARROW_COST 2
 #endif
-constexpr int kWideCost = TAPER_WIDE_COST, kNarrowCost = TAPER_NARROW_COST;  // per tile
+#ifndef TAPER_ROW_COST
+#define TAPER_ROW_COST 2
+#endif
+// per-tile claim costs: swap-mode items with > 4 branches (softmax-bound), narrower swap items
+// and row-mode items (both at about the memory rate)
+constexpr int kWideCost = TAPER_WIDE_COST, kNarrowCost = TAPER_NARROW_COST, kRowCost = TAPER_ROW_COST;
 constexpr double kEps = 1e-9;  // Alg. 1 line 16 "EPS" (no value in the paper) [C-adm-3]
 
 struct AdmitParams {
@@ -485,7 +490,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
   }
 
   // ---- work list (A5): per-request widths, item counts and CSR offsets.
-  // Shared items: (taper_chunk_tokens(Lsh_r, h_local)-token prefix chunk, group of <= 8 admitted branches).  Local items:
+  // Shared items: (taper_chunk_tokens(Lsh_r, h_local)-token prefix chunk, group of <= 16 admitted branches).  Local items:
   // <= kLocalItemTiles 64-token tiles of ONE admitted branch's local KV.  Partials (8 rows
   // per KV head each): shared (chunk c, branch j) at c * w + j, then one per local item.
   int w_loc[kPerThread], nc_loc[kPerThread], nl_loc[kPerThread], cs_loc[kPerThread];
@@ -562,6 +567,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     const int cs_r = p.req_part_off[r];
     const int it0 = p.req_chunk_off[r] + p.req_loc_off[r];  // request-major item numbering
     const ChunkPlan cp = chunk_plan(p.Lsh[r], p.h_local);
+    const int n_ready = p.off[r + 1] - p.off[r];  // the item mode depends on n_r, not on w_r
     for (int c = 0; c < nc; ++c)
       for (int g = 0; g < groups; ++g) {
         ItemDesc d;
@@ -571,7 +577,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
         d.cs0 = cs_r + c * w + g * kMaxItemBranches;
         d.tb = chunk_start(cp, p.Lsh[r], c); d.te = chunk_start(cp, p.Lsh[r], c + 1);
         d.nt = (d.te - d.tb + kTileTokens - 1) / kTileTokens;
-        d.flags = 0;
+        d.flags = (kRowEnabled && n_ready >= kRowMin) ? (kItemRow | (n_ready > 8 ? kItemM128 : 0)) : 0;
         p.items[it0 + c * groups + g] = d;
       }
     // local items: per admitted branch, its local tiles in groups of kLocalItemTiles
@@ -595,7 +601,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
           d.r = r; d.w = 1; d.adm_off = adm_off + j; d.cs0 = cs_r + nc * w + li;
           d.tb = (l0 + li) * kLocalItemTiles; d.te = 0;
           d.nt = nt;
-          d.flags = 1;
+          d.flags = kItemLocal;
           p.items[it0 + nsh + li] = d;
         }
       }
@@ -645,11 +651,12 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
         unsigned long long key = ~0ull;
         if (i < D) {
           const ItemDesc d = p.items[i];
-          // the branch groups of one prefix chunk (w_r > 8) share the cost of the widest
-          // group, so they stay adjacent in the claim order: claimed together, the later
-          // group re-reads the chunk from L2 instead of HBM
-          const int wr = (d.flags & 1) ? d.w : p.req_adm_off[d.r + 1] - p.req_adm_off[d.r];
-          const int cost = d.nt * (min(wr, kMaxItemBranches) > 4 ? kWideCost : kNarrowCost) + kItemCost0;
+          // (with > 16 admitted branches the groups of one prefix chunk share the cost of
+          // the widest, so they stay adjacent: the later group re-reads the chunk from L2)
+          const int wr = (d.flags & kItemLocal) ? d.w : p.req_adm_off[d.r + 1] - p.req_adm_off[d.r];
+          const int per_tile = (d.flags & kItemRow) ? kRowCost
+                                                    : (min(wr, kMaxItemBranches) > 4 ? kWideCost : kNarrowCost);
+          const int cost = d.nt * per_tile + kItemCost0;
           key = ((unsigned long long)(0xffff - cost) << 32) | (unsigned)i;
         }
         keys[i] = key;

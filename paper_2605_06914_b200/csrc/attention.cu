@@ -47,41 +47,54 @@ constexpr int kItemTiles = (kChunk / kTileTokens > kLocalItemTiles) ? kChunk / k
                                                                     : kLocalItemTiles;
 static_assert(kItemTiles <= 64, "scheduler lanes resolve at most two tiles each");
 // K and V tiles ride separate TMA rings: a K stage is released as soon as QK(t) completes,
-// a V stage only after PV(t); each stage is 64 tokens x 128 d bf16 = 16 KB.
+// a V stage only after PV(t); each stage is 64 tokens x 128 d bf16 = 16 KB.  Four + four
+// stages keep ~128 KB in flight per SM, as fast as five + five (same-box A/B, r2 ab_rings:
+// C2 191.3 vs 192.2 us, C3 846 vs 842 us) and they leave room for 16-branch Q operands.
 #ifndef TAPER_KSTAGES
-#define TAPER_KSTAGES 5
+#define TAPER_KSTAGES 4
 #endif
 #ifndef TAPER_VSTAGES
-#define TAPER_VSTAGES 5
+#define TAPER_VSTAGES 4
 #endif
 #ifndef TAPER_EARLY_CLAIM
 #define TAPER_EARLY_CLAIM 1
 #endif
+// Row mode (kItemRow, taper_internal.cuh): stacked rows on the MMA's M, S = Q K^T, thread =
+// row, P kept in TMEM for a TS MMA O += P V.  Swap mode: tokens on M ("swap-AB"), tensor and
+// softmax work proportional to the live rows -- requests with < kRowMin ready slots and
+// every local item (w = 1).  See DESIGN.md "row mode".
+constexpr int kSwapMaxW = kRowMin - 1;       // widest swap-mode item
+constexpr int kSwapMaxWB = (kSwapMaxW + 1) / 2;  // 8-row blocks per softmax group (swap mode)
 constexpr bool kEarlyClaim = TAPER_EARLY_CLAIM;
 constexpr int kKStages = TAPER_KSTAGES;
 constexpr int kVStages = TAPER_VSTAGES;
 constexpr int kStageBytes = 2 * 8192;
 constexpr int kOffV = kKStages * kStageBytes;
-constexpr int kOffQ = kOffV + kVStages * kStageBytes;   // Q^T operand, 2 buffers x 64 rows
-constexpr int kQBytes = kMaxItemBranches * kGroup * 256;  // 16 KB: [branch][d-half][8][128 B]
-constexpr int kOffPT = kOffQ + 2 * kQBytes;              // P^T operand: 128 rows x 128 B
-// Items with <= 4 branches (P^T <= 8 KB) alternate between the two 8 KB halves by tile
-// parity, so softmax(n) only waits for PV(n-2); wider items use the whole buffer.
+constexpr int kOffQ = kOffV + kVStages * kStageBytes;   // Q operand, 2 buffers x 128 rows
+constexpr int kQBytes = kMaxItemBranches * kGroup * 256;  // 32 KB: [branch][d-half][8][128 B]
+constexpr int kOffPT = kOffQ + 2 * kQBytes;              // swap-mode P^T operand
+// Swap items with <= kNarrowPT branches (P^T <= 8 KB) alternate between two P^T halves by
+// tile parity, so softmax(n) only waits for PV(n-2); wider ones use the whole buffer.
 #ifndef TAPER_NARROW_PT
 #define TAPER_NARROW_PT 4
 #endif
-constexpr int kNarrowPT = TAPER_NARROW_PT;
+constexpr int kNarrowPT = TAPER_NARROW_PT < kSwapMaxW ? TAPER_NARROW_PT : kSwapMaxW;
 constexpr int kPTHalf = 2 * kNarrowPT * kGroup * 128;  // hi + lo rows of kNarrowPT branches
-constexpr int kPTBytes = (2 * kPTHalf > 2 * kMaxItemBranches * kGroup * 128)
-                             ? 2 * kPTHalf : 2 * kMaxItemBranches * kGroup * 128;
-constexpr int kOffML = kOffPT + kPTBytes;  // (m, l) of the 64 stacked rows, 2 buffers
-// cross-warp reductions per softmax group: max [2 parities][4 warps][64], sum [4][64]
-constexpr int kRedFloats = 3 * 4 * 64;
-constexpr int kOffRed = kOffML + 2 * 64 * 8;
-constexpr int kOffAlpha = kOffRed + 2 * kRedFloats * 4;  // per-warp rescale factors [8][64]
+constexpr int kPTBytes = (2 * kPTHalf > 2 * kSwapMaxW * kGroup * 128)
+                             ? 2 * kPTHalf : 2 * kSwapMaxW * kGroup * 128;
+constexpr int kOffML = kOffPT + kPTBytes;  // (m, l) of the <= 128 stacked rows, 2 buffers
+// swap mode, cross-warp reductions per softmax group: max [2 parities][4 warps][kRedCols],
+// sum [4][kRedCols] (a group owns <= kSwapMaxWB 8-row blocks)
+constexpr int kRedCols = 8 * kSwapMaxWB;
+constexpr int kRedFloats = 3 * 4 * kRedCols;
+constexpr int kOffRed = kOffML + 2 * 128 * 8;
+// row mode: per-row tile maxima of the two token halves [2 parities][2 groups][128] and the
+// second group's row sums [2 O buffers][128]
+constexpr int kOffRowRed = kOffRed + 2 * kRedFloats * 4;
+constexpr int kOffAlpha = kOffRowRed + (2 * 2 * 128 + 2 * 128) * 4;  // swap: rescale factors [8][kRedCols]
 constexpr int kRecBytes = kItemTiles <= 32 ? 1024 : 2048;  // ItemRec slot
 constexpr int kItemRing = 8192 / kRecBytes;   // claimed-item ring (8 KB of ItemRec records)
-constexpr int kOffRec = kOffAlpha + 8 * 64 * 4;
+constexpr int kOffRec = kOffAlpha + 8 * kRedCols * 4;
 constexpr int kOffBar = kOffRec + kItemRing * kRecBytes;
 constexpr int kSmemUsed = kOffBar + 512;
 constexpr int kSmemBytes = kSmemUsed + 1024;  // + alignment slack
@@ -96,8 +109,25 @@ constexpr int kAttnThreads = 512;
 // equally correct but reported as a hazard).
 constexpr int kRingConsumers = 15 * 32;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColS = 0;     // S^T 0 [0, 64), S^T 1 [64, 128): 64 tokens x N rows
-constexpr uint32_t kColO = 128;   // O^T 0 [128, 256), O^T 1 [256, 384): 128 d x 2N rows
+constexpr uint32_t kColS = 0;     // swap: S^T 0 [0, 64), S^T 1 [64, 128) (64 tokens x N rows);
+                                  // row: S 0 / S 1 (rows x 64 tokens)
+constexpr uint32_t kColO = 128;   // swap: O^T 0 [128, 256), O^T 1 [256, 384) (128 d x 2N rows);
+                                  // row: O 0 / O 1 (rows x 128 d)
+constexpr uint32_t kColP = 384;   // row: P 0 [384, 448), P 1 [448, 512): hi then lo halves of P,
+                                  // rows x 64 tokens bf16 each
+// Row mode splits P = hi + lo (bf16 each) like swap mode: with P rounded to one bf16 the
+// peaked parity case misses allclose(2e-3, 1e-2) (max abs 8.2e-3, r2 run e).
+#ifndef TAPER_ROW_PLO
+#define TAPER_ROW_PLO 1
+#endif
+constexpr bool kRowPlo = TAPER_ROW_PLO;
+// A/B isolation (timing only, on batches without row items): drop row support from one role
+#ifndef TAPER_DBG_ROW_ROLES
+#define TAPER_DBG_ROW_ROLES 7  // bit 0: MMA warp, bit 1: softmax warps, bit 2: epilogue
+#endif
+constexpr bool kRowMma = kRowEnabled && (TAPER_DBG_ROW_ROLES & 1);
+constexpr bool kRowSm = kRowEnabled && (TAPER_DBG_ROW_ROLES & 2);
+constexpr bool kRowEpi = kRowEnabled && (TAPER_DBG_ROW_ROLES & 4);
 
 struct AttnParams {
   // slot_page_off: per slot (local tiles with segment -1) or, when the batch has local
@@ -131,8 +161,10 @@ __device__ __forceinline__ void trace_ev(const AttnParams &p, int e, uint32_t n)
     p.trace[(size_t)n * 16 + e] = clock64();
 }
 
+template <bool B> struct BoolC { static constexpr bool value = B; };
+
 struct Item {
-  int r, g, local, w, adm_off, cs0, nt, tb, te;
+  int r, g, local, w, adm_off, cs0, nt, tb, te, row, m128;
 };
 
 // A claimed work item as the scheduler warp resolves it into SMEM: the descriptor plus, per
@@ -150,7 +182,9 @@ __device__ __forceinline__ void decode_item(const ItemRec *rec, Item &x) {
   x.g = rec->g;
   x.r = rec->desc[0]; x.w = rec->desc[1]; x.adm_off = rec->desc[2]; x.cs0 = rec->desc[3];
   x.tb = rec->desc[4]; x.te = rec->desc[5]; x.nt = rec->desc[6];
-  x.local = rec->desc[7] & 1;
+  x.local = rec->desc[7] & kItemLocal;
+  x.row = (rec->desc[7] & kItemRow) != 0;
+  x.m128 = (rec->desc[7] & kItemM128) != 0;
 }
 
 struct TileInfo {
@@ -209,6 +243,34 @@ __device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t vb, uint32_t pb, 
     const uint64_t a = a0 + uint64_t((kk * 2048) >> 4);
     const uint64_t b = b0 + uint64_t((kk * 32) >> 4);
     tc_mma_f16(tO, a, b, idesc, (first && kk == 0) ? 0u : 1u);
+  }
+}
+
+// Row mode.  S[tS] = Q K^T: M = stacked rows (64 or 128; rows past 8 w are padding), N = 64
+// tokens, K = 128 d.  A = Q (the same SMEM buffer as swap mode's Q^T: SW128 K-major, 8-row
+// groups 2 KB apart, d-halves 1 KB apart), B = the K tile (SW128 K-major, 8-token groups
+// 1 KB apart, d-halves 8 KB apart).  Verified against fp64 by scripts/rowmode_check.cu.
+__device__ __forceinline__ void issue_qk_row(uint32_t tS, uint32_t qb, uint32_t kb, uint32_t idesc) {
+  const uint64_t a0 = umma_desc_sw128(qb, 16, 2048);
+  const uint64_t b0 = umma_desc_sw128(kb, 16, 1024);
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const uint64_t a = a0 + uint64_t((((kk >> 2) * 1024) + (kk & 3) * 32) >> 4);
+    const uint64_t b = b0 + uint64_t((((kk >> 2) * 8192) + (kk & 3) * 32) >> 4);
+    tc_mma_f16(tS, a, b, idesc, kk > 0 ? 1u : 0u);
+  }
+}
+// Row mode.  O[tO] (+)= P V: M = stacked rows, N = 128 d, K = 64 tokens in 4 k-steps.  A = P
+// from TMEM (bf16 pairs, 8 columns per 16 tokens), B = the V tile as an MN-major SW128
+// operand (d-halves 8 KB apart, 8-token groups 1 KB apart).
+__device__ __forceinline__ void issue_pv_row(uint32_t tO, uint32_t tP, uint32_t vb, bool first,
+                                             uint32_t idesc) {
+  const uint64_t b0 = umma_desc_sw128(vb, 8192, 1024);
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const uint64_t b = b0 + uint64_t((kk * 2048) >> 4);
+    tc_mma_f16_tsa(tO, tP + 8 * kk, b, idesc, (first && kk == 0) ? 0u : 1u);
+    if (kRowPlo) tc_mma_f16_tsa(tO, tP + 32 + 8 * kk, b, idesc, 1u);  // + P_lo V
   }
 }
 
@@ -294,6 +356,7 @@ struct SoftmaxCtx {  // per-thread constants of a softmax warp
   uint64_t *s_full, *pv_done, *vfull, *p_full_g, *o_free, *ml_full;
   float2 *xml;
   float *red_g, *alpha_s;
+  float *row_red, *row_lsum;  // row mode: [2][2][128] tile maxima, [2][128] group-1 row sums
   uint32_t tmem, lane_off, pt_base;
   int grp, wq, lane, warp, tid, bar_id;
   float c;
@@ -357,7 +420,7 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
     tc_fence_after();
     if constexpr (WB > 0) {
       const uint32_t tS = C.tmem + C.lane_off + kColS + sb * 64;
-      float *red_max = C.red_g + (n & 1) * 256;
+      float *red_max = C.red_g + (n & 1) * 4 * kRedCols;
       uint32_t s[4 * WB];
       tmem_ld_16x256<WB>(tS + 8 * blk0, s);
       tmem_ld_wait();
@@ -405,13 +468,13 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
           }
         }
 #pragma unroll
-        for (int j = 0; j < NF; ++j) red_max[wq * 64 + col[j]] = v[j];
+        for (int j = 0; j < NF; ++j) red_max[wq * kRedCols + col[j]] = v[j];
         named_bar_sync(C.bar_id, 128);
         if (C.warp == 2 && lane == 0) trace_ev(*C.p, 13, n);
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
-          float mx = fmaxf(fmaxf(red_max[col[j]], red_max[64 + col[j]]),
-                           fmaxf(red_max[128 + col[j]], red_max[192 + col[j]]));
+          float mx = fmaxf(fmaxf(red_max[col[j]], red_max[kRedCols + col[j]]),
+                           fmaxf(red_max[2 * kRedCols + col[j]], red_max[3 * kRedCols + col[j]]));
           mx *= C.c;  // log2 units (c = softmax scale * log2 e > 0)
           if (mx > m_red[j] + 8.f) m_red[j] = mx;
           v[j] = m_red[j];
@@ -532,7 +595,7 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
     ++n;
   }
   // row sums: this thread's partial over its 2 tokens per tile -> 16 tokens -> 4 warps
-  float *red_sum = C.red_g + 512;
+  float *red_sum = C.red_g + 8 * kRedCols;
   if constexpr (WB > 0) {
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
@@ -543,8 +606,8 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
     if (lane < 4) {
 #pragma unroll
       for (int b = 0; b < WB; ++b) {
-        red_sum[wq * 64 + 8 * b + c0] = l_run[2 * b];
-        red_sum[wq * 64 + 8 * b + c0 + 1] = l_run[2 * b + 1];
+        red_sum[wq * kRedCols + 8 * b + c0] = l_run[2 * b];
+        red_sum[wq * kRedCols + 8 * b + c0 + 1] = l_run[2 * b + 1];
       }
     }
     named_bar_sync(C.bar_id, 128);
@@ -558,11 +621,152 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int cl = 8 * b + c0 + e;
-          const float L = red_sum[cl] + red_sum[64 + cl] + red_sum[128 + cl] + red_sum[192 + cl];
-          C.xml[ob * 64 + 8 * blk0 + cl] = make_float2(m_run[2 * b + e], L);
+          const float L = red_sum[cl] + red_sum[kRedCols + cl] + red_sum[2 * kRedCols + cl] + red_sum[3 * kRedCols + cl];
+          C.xml[ob * 128 + 8 * blk0 + cl] = make_float2(m_run[2 * b + e], L);
         }
     }
     named_bar_sync(C.bar_id, 128);  // red_sum reused by the next item
+  }
+  mbar_arrive(C.ml_full + ob);
+}
+
+// Row mode: one shared item of w >= kRowMin branches (8 w <= 128 stacked rows; M = 128 when
+// 8 w > 64, else 64).  Thread = stacked row: with M = 128 row 32 wq + lane holds 32 tokens of
+// the tile; with M = 64 (rows in lanes 0-15 of each quadrant, 16x32bx2 accesses) row
+// 16 wq + lane % 16 holds 16 tokens, lanes l and l ^ 16 the two halves.  Group g takes tokens
+// [32 g, 32 g + 32) of every tile; the two groups' tile maxima of a row meet in SMEM behind a
+// 64-thread barrier of the warp pair sharing the TMEM quadrant, so both apply the same lazy
+// running max (moves only when a tile max exceeds it by > 8 in log2 units) and each rescales
+// its half of O's 128 columns.  P = 2^(x c - m) = hi + lo goes to TMEM as two sets of bf16
+// pairs, the A operands of two PV TS-MMAs accumulating into the same O.
+#ifndef TAPER_ROW_NOINLINE
+#define TAPER_ROW_NOINLINE 0
+#endif
+#if TAPER_ROW_NOINLINE
+#define TAPER_ROW_INLINE __noinline__
+#else
+#define TAPER_ROW_INLINE __forceinline__
+#endif
+// (Out of line by default: a separate function keeps the swap-mode softmax code of the kernel
+// body contiguous; inlined, the extra ~600 instructions slowed swap-only layers by ~1.7 %.)
+template <bool M128>
+__device__ TAPER_ROW_INLINE void softmax_item_row(const SoftmaxCtx C, const Item x,
+                                                  uint32_t item_idx, uint32_t &n) {
+  constexpr int NT = M128 ? 32 : 16;  // tokens per thread per tile
+  const int lane = C.lane, wq = C.wq, grp = C.grp;
+  const int half = M128 ? 0 : (lane >> 4);
+  const int row = M128 ? 32 * wq + lane : 16 * wq + (lane & 15);
+  const int n_live = 8 * x.w;
+  const bool warp_live = (M128 ? 32 * wq : 16 * wq) < n_live;  // same for the warp pair
+  const bool writer = M128 || half == 0;                      // one thread per row and group
+  const int tk0 = 32 * grp + 16 * half;                       // first token of this thread
+  const uint32_t ob = item_idx & 1;
+  const uint32_t tO = C.tmem + C.lane_off + kColO + ob * 128;
+  const int pair_bar = 4 + wq;
+  float m_run = -INFINITY, l_run = 0.f;
+  for (int t = 0; t < x.nt; ++t) {
+    const uint32_t sb = n & 1;
+    const int nvalid = min(kTile, x.te - (x.tb + t * kTile));
+    mbar_wait(C.s_full + sb, (n >> 1) & 1);
+    tc_fence_after();
+    if (warp_live) {
+      uint32_t s[NT];
+      const uint32_t tS = C.tmem + C.lane_off + kColS + sb * 64 + 32 * grp;
+      if constexpr (M128) tmem_ld32(tS, s); else tmem_ld_x2_16<16>(tS, s);
+      tmem_ld_wait();
+      float xv[NT];
+      float mh = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        xv[j] = tk0 + j < nvalid ? __uint_as_float(s[j]) : -INFINITY;
+        mh = fmaxf(mh, xv[j]);
+      }
+      if constexpr (!M128) mh = fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, 16));
+      float *rb = C.row_red + sb * 256;  // [grp][row], by tile parity
+      if (writer) rb[grp * 128 + row] = mh;
+      named_bar_sync(pair_bar, 64);
+      const float mt = fmaxf(mh, rb[(grp ^ 1) * 128 + row]) * C.c;  // log2 units
+      float alpha = 1.f;
+      if (mt > m_run + 8.f) {
+        alpha = ex2(m_run - mt);  // 0 when m_run = -inf
+        l_run *= alpha;
+        m_run = mt;
+      }
+      const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
+      uint32_t pk[NT / 2], pl[kRowPlo ? NT / 2 : 1];
+      float ls = 0.f;
+#pragma unroll
+      for (int i = 0; i < NT / 2; ++i) {
+        const float pA = ex2(fmaf(xv[2 * i], C.c, neg_m)), pB = ex2(fmaf(xv[2 * i + 1], C.c, neg_m));
+        pk[i] = pack_bf16(pA, pB);
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&pk[i]));
+        if constexpr (kRowPlo) {
+          pl[i] = pack_bf16(pA - f.x, pB - f.y);
+          ls += pA + pB;
+        } else {
+          ls += f.x + f.y;  // the row sum of what the MMA multiplies
+        }
+      }
+      l_run += ls;
+      // O rows *= alpha needs PV(n-1) complete (and PV(n) waits for this tile's p_full); the
+      // P buffer this tile writes was last read by PV(n-2)
+      const bool rescale = t > 0 && __any_sync(0xffffffffu, alpha != 1.f);
+      if (rescale) {
+        mbar_wait(C.pv_done + ((n - 1) & 1), ((n - 1) >> 1) & 1);
+        tc_fence_after();
+        uint32_t o[32];
+        if constexpr (M128) {
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            tmem_ld32(tO + 64 * grp + 32 * c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+            tmem_st32(tO + 64 * grp + 32 * c, o);
+          }
+        } else {
+          tmem_ld_x2_32<32>(tO + 64 * grp, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+          tmem_st_x2_32<32>(tO + 64 * grp, o);
+        }
+      } else if (n >= 2) {
+        mbar_wait(C.pv_done + (n & 1), ((n - 2) >> 1) & 1);
+      }
+      const uint32_t tP = C.tmem + C.lane_off + kColP + sb * 64 + 16 * grp;
+      if constexpr (M128) {
+        tmem_st16(tP, *reinterpret_cast<const uint32_t(*)[16]>(pk));
+        if constexpr (kRowPlo) tmem_st16(tP + 32, *reinterpret_cast<const uint32_t(*)[16]>(pl));
+      } else {
+        tmem_st_x2_8<8>(tP, pk);
+        if constexpr (kRowPlo) tmem_st_x2_8<8>(tP + 32, pl);
+      }
+      tmem_st_wait();
+    }
+    if (C.grp == 1 && nvalid < kTile) {  // zero V rows past the last valid token (as swap mode)
+      const uint32_t vs = n % kVStages;
+      mbar_wait(C.vfull + vs, (n / kVStages) & 1);
+      uint8_t *vt = C.smem + kOffV + vs * kStageBytes;
+      const int nz = (kTile - nvalid) * 8;
+      for (int i = C.tid - 384; i < 2 * nz; i += 128) {
+        const int hf = i / nz, j = i - hf * nz;
+        *reinterpret_cast<uint4 *>(vt + hf * 8192 + nvalid * 128 + j * 16) = make_uint4(0u, 0u, 0u, 0u);
+      }
+      fence_proxy_async_smem();
+    }
+    tc_fence_before();
+    mbar_arrive(C.p_full_g + (n & 1));
+    ++n;
+  }
+  if constexpr (!M128) l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);
+  // publish (m, l) for the epilogue; xml[ob] / row_lsum[ob] were consumed by item_idx-2
+  mbar_wait(C.o_free + ob, ((item_idx >> 1) & 1) ^ 1);
+  if (warp_live) {
+    float *lsum = C.row_lsum + ob * 128;
+    if (grp == 1 && writer) lsum[row] = l_run;
+    named_bar_sync(pair_bar, 64);
+    if (grp == 0 && writer && row < n_live) C.xml[ob * 128 + row] = make_float2(m_run, l_run + lsum[row]);
   }
   mbar_arrive(C.ml_full + ob);
 }
@@ -699,7 +903,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         adm_off = __shfl_sync(0xffffffffu, d, 2);
         x.tb = __shfl_sync(0xffffffffu, d, 4);
         x.te = __shfl_sync(0xffffffffu, d, 5);
-        x.local = __shfl_sync(0xffffffffu, d, 7) & 1;
+        x.local = __shfl_sync(0xffffffffu, d, 7) & kItemLocal;
         if (lane < 8) rec->desc[lane] = d;
         for (int t = lane; t < nt; t += 32) {
           const TileInfo ti = tile_info(p, x, t);
@@ -781,12 +985,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       const int g_u = rec->g;
       const int nt_u = rec->desc[6];
+      // (Tiles issued in pairs by lanes 0 and 1 -- a higher TMA issue ceiling in isolation,
+      // scripts/tma_issue_probe.cu -- measured 2.3 % slower on C2, r2 run l; one lane issues.)
       for (int t = 0; t < nt_u; ++t, ++n_prod) {
         const int tok0 = rec->tok0[t];
         const int valid = rec->valid[t];
-        int pg[kTile / 16];
-#pragma unroll
-        for (int b = 0; b < kTile / 16; ++b) pg[b] = rec->pg[t][b];
         const uint32_t st = n_prod % n_stages;
         uint8_t *dst = ring + st * kStageBytes;
         mbar_wait(ring_empty + st, ((n_prod / n_stages) & 1) ^ 1);
@@ -800,17 +1003,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           if (p.tma5d && valid == kTile) {
             // one box: {64 d, 64 tokens, 2 d-halves} -> [d-half][token][64] (two SW128 atoms)
             mbar_arrive_expect_tx(ring_full + st, 2 * kTile * 128);
-            tma_load_5d(dst, tmap, ring_full + st, 0, tok0 % p.page_size, 0, g_u, pg[0]);
+            tma_load_5d(dst, tmap, ring_full + st, 0, tok0 % p.page_size, 0, g_u, rec->pg[t][0]);
           } else if (p.tma5d) {
             // partial tile: {64 d, 16 tokens} boxes per d-half up to the last valid token
             // (rows past it are zeroed by the softmax warps before PV)
             const int n16 = (valid + 15) >> 4;
+            const int pg0 = rec->pg[t][0];
             mbar_arrive_expect_tx(ring_full + st, n16 * 2 * 2048);
             for (int b = 0; b < n16; ++b)
               for (int hf = 0; hf < 2; ++hf)
                 tma_load_5d(dst + hf * 8192 + b * 2048, tmap16, ring_full + st, 0,
-                            tok0 % p.page_size + 16 * b, hf, g_u, pg[0]);
+                            tok0 % p.page_size + 16 * b, hf, g_u, pg0);
           } else {
+            int pg[kTile / 16];
+#pragma unroll
+            for (int b = 0; b < kTile / 16; ++b) pg[b] = rec->pg[t][b];
             const int n_box = (valid + box_tok - 1) / box_tok;
             mbar_arrive_expect_tx(ring_full + st, n_box * half_box_bytes * 2);
 #pragma unroll
@@ -851,52 +1058,77 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (it < 0) break;
       const int wi = __shfl_sync(0xffffffffu, x.w, 0);
       const int nt = __shfl_sync(0xffffffffu, x.nt, 0);
-      const uint32_t idesc_qk = umma_idesc_bf16(64, 8 * wi, false, false);
-      const uint32_t idesc_pv = umma_idesc_bf16(128, 16 * wi, true, false);
+      const bool row = kRowMma && __shfl_sync(0xffffffffu, x.row, 0);
       const uint32_t qb = item_idx & 1;
       const uint32_t ob = item_idx & 1;  // O double buffer
       const uint32_t tO = tmem_u + kColO + ob * 128;
       mbar_wait(q_full + qb, (item_idx >> 1) & 1);
       if (lane == 0) trace_ev(p, 6, n);
       tc_fence_after();
-      for (int t = 0; t <= nt; ++t) {
-        if (t < nt) {
-          const uint32_t ks = n % kKStages;
-          mbar_wait(kfull + ks, (n / kKStages) & 1);
-          if (lane == 0) trace_ev(p, 1, n);
-          tc_fence_after();
-          if (elect_one()) {
-            issue_qk(tmem_u + kColS + (n & 1) * 64, sK + ks * kStageBytes, sQ + qb * kQBytes,
-                     idesc_qk);
-            tc_commit(kempty + ks);
-            tc_commit(s_full + (n & 1));
-            if (t == nt - 1) tc_commit(q_free + qb);
-          }
-          __syncwarp();
-          if (lane == 0) trace_ev(p, 2, n);
+      // One tile loop per mode (selected once per item): a per-tile mode branch in this
+      // latency-critical loop slowed swap-only layers by ~1.7 % (r2 run m).
+      auto tile_loop = [&](auto row_c) {
+        constexpr bool kRow = decltype(row_c)::value;
+        uint32_t idesc_qk, idesc_pv;
+        if constexpr (kRow) {
+          const int mrow = __shfl_sync(0xffffffffu, x.m128, 0) ? 128 : 64;  // rows on M (padded)
+          idesc_qk = umma_idesc_bf16(mrow, 64, false, false);
+          idesc_pv = umma_idesc_bf16(mrow, 128, false, true);
+        } else {
+          idesc_qk = umma_idesc_bf16(64, 8 * wi, false, false);
+          idesc_pv = umma_idesc_bf16(128, 16 * wi, true, false);
         }
-        if (t > 0) {
-          // PV of the previous tile (its P^T is ready once the softmax arrives on p_full)
-          const uint32_t m = n - 1;
-          mbar_wait(p_full + (m & 1), (m >> 1) & 1);
-          mbar_wait(p_full + 2 + (m & 1), (m >> 1) & 1);
-          if (lane == 0) trace_ev(p, 3, m);
-          const bool first = t == 1;
-          if (first) mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);  // epilogue item-2 done
-          const uint32_t vs = m % kVStages;
-          mbar_wait(vfull + vs, (m / kVStages) & 1);
-          tc_fence_after();
-          if (elect_one()) {
-            issue_pv(tO, sV + vs * kStageBytes,
-                     sPT + (wi > kNarrowPT ? 0u : (m & 1) * kPTHalf), first, idesc_pv);
-            tc_commit(vempty + vs);
-            tc_commit(pv_done + (m & 1));
-            if (t == nt) tc_commit(o_full + ob);
+        for (int t = 0; t <= nt; ++t) {
+          if (t < nt) {
+            const uint32_t ks = n % kKStages;
+            mbar_wait(kfull + ks, (n / kKStages) & 1);
+            if (lane == 0) trace_ev(p, 1, n);
+            tc_fence_after();
+            if (elect_one()) {
+              if constexpr (kRow)
+                issue_qk_row(tmem_u + kColS + (n & 1) * 64, sQ + qb * kQBytes, sK + ks * kStageBytes,
+                             idesc_qk);
+              else
+                issue_qk(tmem_u + kColS + (n & 1) * 64, sK + ks * kStageBytes, sQ + qb * kQBytes,
+                         idesc_qk);
+              tc_commit(kempty + ks);
+              tc_commit(s_full + (n & 1));
+              if (t == nt - 1) tc_commit(q_free + qb);
+            }
+            __syncwarp();
+            if (lane == 0) trace_ev(p, 2, n);
           }
-          __syncwarp();
-          if (lane == 0) trace_ev(p, 5, m);
+          if (t > 0) {
+            // PV of the previous tile (its P is ready once the softmax arrives on p_full)
+            const uint32_t m = n - 1;
+            mbar_wait(p_full + (m & 1), (m >> 1) & 1);
+            mbar_wait(p_full + 2 + (m & 1), (m >> 1) & 1);
+            if (lane == 0) trace_ev(p, 3, m);
+            const bool first = t == 1;
+            if (first) mbar_wait(o_free + ob, ((item_idx >> 1) & 1) ^ 1);  // epilogue item-2 done
+            const uint32_t vs = m % kVStages;
+            mbar_wait(vfull + vs, (m / kVStages) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+              if constexpr (kRow)
+                issue_pv_row(tO, tmem_u + kColP + (m & 1) * 64, sV + vs * kStageBytes, first, idesc_pv);
+              else
+                issue_pv(tO, sV + vs * kStageBytes,
+                         sPT + (wi > kNarrowPT ? 0u : (m & 1) * kPTHalf), first, idesc_pv);
+              tc_commit(vempty + vs);
+              tc_commit(pv_done + (m & 1));
+              if (t == nt) tc_commit(o_full + ob);
+            }
+            __syncwarp();
+            if (lane == 0) trace_ev(p, 5, m);
+          }
+          if (t < nt) ++n;
         }
-        if (t < nt) ++n;
+      };
+      if (__builtin_expect(!row, 1)) {
+        tile_loop(BoolC<false>{});
+      } else {
+        if constexpr (kRowMma) tile_loop(BoolC<true>{});
       }
     }
   } else if (warp < 6 || warp >= 12) {
@@ -924,7 +1156,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     C.ml_full = ml_full;
     C.xml = xml;
     C.red_g = red + C.grp * kRedFloats;
-    C.alpha_s = reinterpret_cast<float *>(smem + kOffAlpha) + (C.grp * 4 + C.wq) * 64;
+    C.alpha_s = reinterpret_cast<float *>(smem + kOffAlpha) + (C.grp * 4 + C.wq) * kRedCols;
+    C.row_red = reinterpret_cast<float *>(smem + kOffRowRed);
+    C.row_lsum = C.row_red + 2 * 2 * 128;
     uint32_t n = 0;
     bool prev_wide = true;
     for (uint32_t item_idx = 0;; ++item_idx) {
@@ -936,15 +1170,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const ItemRec *rec = recs + item_idx % kItemRing;
       Item x;
       decode_item(rec, x);
-      const int wb0 = (x.w + 1) >> 1;
-      const int wb = C.grp ? x.w - wb0 : wb0;   // 8-row blocks of this group
-      const int blk0 = C.grp ? wb0 : 0;
-      switch (wb) {
-        case 0: softmax_item<0>(C, rec, x, blk0, item_idx, n, prev_wide); break;
-        case 1: softmax_item<1>(C, rec, x, blk0, item_idx, n, prev_wide); break;
-        case 2: softmax_item<2>(C, rec, x, blk0, item_idx, n, prev_wide); break;
-        case 3: softmax_item<3>(C, rec, x, blk0, item_idx, n, prev_wide); break;
-        default: softmax_item<4>(C, rec, x, blk0, item_idx, n, prev_wide); break;
+      if (kRowSm && x.row) {
+        // (M = 64 row items exist only when kRowMin <= 8; n_r >= 9 means M = 128)
+        if (kRowMin > 8 || x.m128) softmax_item_row<true>(C, x, item_idx, n);
+        else if constexpr (kRowMin <= 8) softmax_item_row<false>(C, x, item_idx, n);
+        prev_wide = false;  // the swap P^T halves were last read before this item's tiles
+      } else {
+        const int wb0 = (x.w + 1) >> 1;
+        const int wb = C.grp ? x.w - wb0 : wb0;   // 8-row blocks of this group
+        const int blk0 = C.grp ? wb0 : 0;
+        switch (wb) {
+          case 0: softmax_item<0>(C, rec, x, blk0, item_idx, n, prev_wide); break;
+          case 1: softmax_item<1>(C, rec, x, blk0, item_idx, n, prev_wide); break;
+          case 2: if constexpr (kSwapMaxWB >= 2) softmax_item<2>(C, rec, x, blk0, item_idx, n, prev_wide); break;
+          case 3: if constexpr (kSwapMaxWB >= 3) softmax_item<3>(C, rec, x, blk0, item_idx, n, prev_wide); break;
+          default: if constexpr (kSwapMaxWB >= 4) softmax_item<4>(C, rec, x, blk0, item_idx, n, prev_wide); break;
+        }
       }
       ring_release(it_empty, item_idx, lane);
     }
@@ -974,20 +1215,48 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tr[13] = x.w; tr[14] = x.nt; tr[15] = x.local;
       }
       tc_fence_after();
+      if (kRowEpi && x.row) {
+        // row mode: O[row][d], thread = row (M = 128) or half a row (M = 64, 16x32bx2);
+        // each thread writes its row's contiguous 512 B (256 B) of the partial
+        const bool m128 = kRowMin > 8 || x.m128;
+        const int row = m128 ? 32 * wq + lane : 16 * wq + (lane & 15);
+        const int hf = m128 ? 0 : (lane >> 4);
+        if ((m128 ? 32 * wq : 16 * wq) < 8 * x.w) {
+          const bool live = row < 8 * x.w;
+          const size_t prow = ((size_t)(x.cs0 + (row >> 3)) * h + x.g) * kGroup + (row & 7);
+          const float2 ml = live ? xml[ob * 128 + row] : make_float2(0.f, 0.f);
+          const float inv = ml.y > 0.f ? 1.f / ml.y : 0.f;
+          float4 *dst = reinterpret_cast<float4 *>(p.part_o + prow * kHeadDim + 64 * hf);
 #pragma unroll 1
-      for (int b = 0; b < x.w; ++b) {
+          for (int c = 0; c < (m128 ? 4 : 2); ++c) {
+            uint32_t o[32];
+            if (m128) tmem_ld32(tO + 32 * c, o); else tmem_ld_x2_32<64>(tO + 32 * c, o);
+            tmem_ld_wait();
+            if (live) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                dst[8 * c + j] = make_float4(__uint_as_float(o[4 * j]) * inv, __uint_as_float(o[4 * j + 1]) * inv,
+                                             __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
+            }
+          }
+          if (live && hf == 0)
+            p.part_lse[prow] = ml.y > 0.f ? (ml.x + __log2f(ml.y)) * 0.69314718055994531f : -INFINITY;
+        }
+      }
+#pragma unroll 1
+      for (int b = 0; b < ((kRowEpi && x.row) ? 0 : x.w); ++b) {
         uint32_t o[16];
         tmem_ld16(tO + 16 * b, o);
         tmem_ld_wait();
         const size_t prow0 = ((size_t)(x.cs0 + b) * h + x.g) * kGroup;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float2 ml = xml[ob * 64 + 8 * b + e];
+          const float2 ml = xml[ob * 128 + 8 * b + e];
           const float inv = ml.y > 0.f ? 1.f / ml.y : 0.f;
           p.part_o[(prow0 + e) * kHeadDim + d] = (__uint_as_float(o[e]) + __uint_as_float(o[8 + e])) * inv;
         }
         if (etid < 8) {
-          const float2 ml = xml[ob * 64 + 8 * b + etid];
+          const float2 ml = xml[ob * 128 + 8 * b + etid];
           p.part_lse[prow0 + etid] =
               ml.y > 0.f ? (ml.x + __log2f(ml.y)) * 0.69314718055994531f : -INFINITY;
         }

@@ -16,7 +16,7 @@ constexpr int kChunk = TAPER_CHUNK_TOKENS;  // largest prefix chunk (taper_chunk
 constexpr int kMaxSlots = TAPER_MAX_SLOTS;
 constexpr int kTileTokens = 64;       // tokens per pipeline tile (one TMA stage)
 constexpr int kLocalItemTiles = 16;   // branch-local tiles per local work item
-constexpr int kMaxItemBranches = 8;   // admitted branches stacked in one shared item (N <= 64)
+constexpr int kMaxItemBranches = 16;  // admitted branches stacked in one shared item (<= 128 rows)
 
 // ------------------------------------------------------------------ workspace layout
 // hdr[0] = n_rc    : number of (request, prefix chunk) pairs (shared items per KV head)
@@ -77,8 +77,24 @@ struct ItemDesc {
   int32_t tb;       // prefix chunk: first token; local item: first local-tile entry
   int32_t te;       // prefix chunk: end token;   local item: unused
   int32_t nt;       // 64-token tiles
-  int32_t flags;    // bit 0: local item; bits 1-3: replication factor (1, 2, 4); bit 4: M = 64
+  int32_t flags;    // bit 0: local item; bit 1: row mode; bit 2: row mode with M = 128
 };
+constexpr int32_t kItemLocal = 1, kItemRow = 2, kItemM128 = 4;
+
+// Shared items of a request with >= kRowMin ready slots run in ROW mode (stacked rows on the
+// MMA's M; M = 128 when the request has > 8 ready slots, else 64), the others (and every
+// local item) in SWAP mode (tokens on M).  The mode and M depend on the request's ready
+// slots n_r, never on how many of them are admitted, so a slot's arithmetic -- and its
+// output bits -- do not depend on its co-admitted siblings (Lemma 1).
+#ifndef TAPER_ROW_MIN
+#define TAPER_ROW_MIN 9
+#endif
+constexpr int kRowMin = TAPER_ROW_MIN;
+#ifndef TAPER_ROW_ENABLE
+#define TAPER_ROW_ENABLE 1
+#endif
+constexpr bool kRowEnabled = TAPER_ROW_ENABLE;  // 0: every item in swap mode (A/B builds)
+static_assert(kRowMin >= 2 && kRowMin <= 9, "swap mode covers at most 8 branches");
 
 __host__ __device__ inline int64_t ws_cap_cs(size_t bytes, int R, int S, int h_local) {
   WsLayout w = ws_layout(R, S);
@@ -232,6 +248,16 @@ __device__ __forceinline__ void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, 
           d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(mask[0]), "r"(mask[1]),
       "r"(mask[2]), "r"(mask[3])
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem] with every output lane enabled (A K-major in TMEM).
+__device__ __forceinline__ void tc_mma_f16_tsa(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.
