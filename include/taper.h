@@ -75,25 +75,29 @@ extern "C" {
 #ifndef TAPER_CHUNK_TOKENS
 #define TAPER_CHUNK_TOKENS 4096 /* largest shared-prefix split (one work item's span)    */
 #endif
-/* Shared-prefix split of request r on a rank holding h_local KV heads: chunks of
- *     clamp(roundup_64(max(512 * h_local, Lsh_r / 8)), 1024, TAPER_CHUNK_TOKENS)
- * tokens -- 4096 for a 4k prefix at h_local = 8, 1024 at h_local <= 2, longer prefixes keep
- * longer chunks (fewer partials) -- so a rank's work items stay plentiful when G > 1 GPUs
- * split the heads (measured: DESIGN.md).  Chunk boundaries depend only on Lsh_r and
- * h_local, never on which branches, siblings or other requests are admitted (schedule
- * invariance, Lemma 1).                                                         */
+/* Shared-prefix split of request r on a rank holding h_local KV heads, in a batch of n_req
+ * requests: chunks of
+ *     clamp(roundup_64(Lsh_r * h_local * n_req / TAPER_CHUNK_TARGET), 1024, TAPER_CHUNK_TOKENS)
+ * tokens, i.e. about TAPER_CHUNK_TARGET shared work items per rank whatever the batch (a few
+ * per SM of the 148: enough to balance the dynamic schedule, few enough to amortise each
+ * item's Q load and partial) -- 4096 for the C2 step at h_local = 8, 1024 at h_local = 1; a
+ * 32-request long-context batch splits its 16-32k prefixes finer than a 256-request one.
+ * Chunk boundaries depend only on Lsh_r, h_local and n_req, never on which branches are
+ * admitted (schedule invariance, Lemma 1); the split is finest at h_local = 1.    */
 #if defined(__CUDACC__)
 #define TAPER_HD __host__ __device__
 #else
 #define TAPER_HD
 #endif
-static inline TAPER_HD int32_t taper_chunk_tokens(int32_t lsh, int32_t h_local) {
-  int32_t c = 512 * h_local;
-  if (lsh / 8 > c) c = lsh / 8;
+#ifndef TAPER_CHUNK_TARGET
+#define TAPER_CHUNK_TARGET 512
+#endif
+static inline TAPER_HD int32_t taper_chunk_tokens(int32_t lsh, int32_t h_local, int32_t n_req) {
+  int64_t c = (int64_t)lsh * h_local * n_req / TAPER_CHUNK_TARGET;
   c = (c + 63) / 64 * 64;
   if (c < 1024) c = 1024;
   if (c > TAPER_CHUNK_TOKENS) c = TAPER_CHUNK_TOKENS;
-  return c;
+  return (int32_t)c;
 }
 
 /* App. C.1 display eq. (L316): T(S) = a + b*n_tokens + c*L_context, in ms. [host]      */
@@ -191,7 +195,7 @@ typedef struct {
 
 /* Workspace bytes for a batch of at most n_req requests / n_slot slots on a rank with
  * h_local KV heads.  max_chunk_slots bounds the partial rows' count
- *     sum_r w_r * ceil(Lsh_r / taper_chunk_tokens(Lsh_r, h_local))  +  sum_{s admitted} ceil(Lloc_s / 1024)
+ *     sum_r w_r * ceil(Lsh_r / taper_chunk_tokens(Lsh_r, h_local, n_req))  +  sum_{s admitted} ceil(Lloc_s / 1024)
  * (prefix chunks per admitted branch, plus one per local item of <= 16 64-token tiles;
  * with local segments the second sum runs over segments: sum ceil(seg_len / 1024));
  * the Eager value of that sum over all ready slots is always enough.  An undersized
@@ -202,7 +206,7 @@ TAPER_API int taper_workspace_size(int32_t n_req, int32_t n_slot, int32_t h_loca
 /* The Eager bound of max_chunk_slots above, computed from HOST copies of the batch
  * arrays (req_shared_len [R], req_slot_off [R+1], slot_local_len [S]; slot_seg_off /
  * seg_len or NULL): every ready slot admitted, prefix chunks of
- * taper_chunk_tokens(Lsh_r, h_local) tokens.  A bound for h_local = 1 holds for every
+ * taper_chunk_tokens(Lsh_r, h_local, n_req) tokens.  A bound for h_local = 1 holds for every
  * h_local (the finest split).  Errors: TAPER_ERR_ARG (null array, non-monotone CSR,
  * negative length).  [host]                                                            */
 TAPER_API int taper_max_chunk_slots(int32_t n_req, int32_t n_slot,

@@ -77,7 +77,7 @@ __device__ __forceinline__ int local_items(const AdmitParams &p, int s) {
 }
 
 // Prefix chunks of a request (a function of Lsh and h_local only: schedule invariance,
-// Lemma 1).  Nominal chunks of ck = taper_chunk_tokens(Lsh, h) tokens; with >= 3 chunks and
+// Lemma 1).  Nominal chunks of ck = taper_chunk_tokens(Lsh, h, R) tokens; with >= 3 chunks and
 // TAPER_SKEW_CHUNKS, the first is ck + ck/2 and the others shift by ck/2, so the last one is
 // about half a chunk: the longest-first claim order then ends on short items.  Chunk starts
 // stay multiples of 64 tokens (a tile never straddles a page).
@@ -85,9 +85,9 @@ __device__ __forceinline__ int local_items(const AdmitParams &p, int s) {
 #define TAPER_SKEW_CHUNKS 0
 #endif
 struct ChunkPlan { int ck, half, n; bool skew; };
-__device__ __forceinline__ ChunkPlan chunk_plan(int lsh, int h) {
+__device__ __forceinline__ ChunkPlan chunk_plan(int lsh, int h, int R) {
   ChunkPlan c;
-  c.ck = taper_chunk_tokens(lsh, h);
+  c.ck = taper_chunk_tokens(lsh, h, R);
   c.half = (c.ck / 2) / kTileTokens * kTileTokens;
   const int n = (lsh + c.ck - 1) / c.ck;
   c.skew = TAPER_SKEW_CHUNKS && n >= 3 && c.ck + c.half <= kChunk;
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
   }
 
   // ---- work list (A5): per-request widths, item counts and CSR offsets.
-  // Shared items: (taper_chunk_tokens(Lsh_r, h_local)-token prefix chunk, group of <= 16 admitted branches).  Local items:
+  // Shared items: (taper_chunk_tokens(Lsh_r, h_local, R)-token prefix chunk, group of <= 16 admitted branches).  Local items:
   // <= kLocalItemTiles 64-token tiles of ONE admitted branch's local KV.  Partials (8 rows
   // per KV head each): shared (chunk c, branch j) at c * w + j, then one per local item.
   int w_loc[kPerThread], nc_loc[kPerThread], nl_loc[kPerThread], cs_loc[kPerThread];
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
             w += 1;
             nl += local_items(p, s);
           }
-        if (w > 0 && p.Lsh[r] > 0) nc = chunk_plan(p.Lsh[r], p.h_local).n;
+        if (w > 0 && p.Lsh[r] > 0) nc = chunk_plan(p.Lsh[r], p.h_local, R).n;
       }
       p.req_width[r] = w;
     }
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     const int nc = nsh / groups;
     const int cs_r = p.req_part_off[r];
     const int it0 = p.req_chunk_off[r] + p.req_loc_off[r];  // request-major item numbering
-    const ChunkPlan cp = chunk_plan(p.Lsh[r], p.h_local);
+    const ChunkPlan cp = chunk_plan(p.Lsh[r], p.h_local, R);
     const int n_ready = p.off[r + 1] - p.off[r];  // the item mode depends on n_r, not on w_r
     for (int c = 0; c < nc; ++c)
       for (int g = 0; g < groups; ++g) {

@@ -78,7 +78,7 @@ extern "C" int taper_max_chunk_slots(int32_t n_req, int32_t n_slot, const int32_
   for (int r = 0; r < n_req; ++r) {
     if (off[r + 1] < off[r] || lsh[r] < 0)
       return taper::fail(TAPER_ERR_ARG, "non-monotone req_slot_off or negative length");
-    const int64_t ck = taper_chunk_tokens(lsh[r], h_local);
+    const int64_t ck = taper_chunk_tokens(lsh[r], h_local, n_req);
     total += int64_t(off[r + 1] - off[r]) * ((int64_t(lsh[r]) + ck - 1) / ck);
   }
   for (int s = 0; s < n_slot; ++s) {

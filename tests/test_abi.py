@@ -40,15 +40,19 @@ def test_host_validation_without_gpu():
         T.taper_workspace_size(10, 10, 9, 1)
     assert "monotone" in T.taper_status_string(-3)
     assert "precision" in T.taper_status_string(4)
-    # 4096-token prefix chunks x ready branches (3 x 1 + 1 x 1 + 2 x 0) + one local item per
-    # branch with local tokens (65, 1, 2, 3 -> 4 items of <= 16 x 64 tokens)
-    assert T.max_chunk_slots([4097, 1, 0], [0, 3, 4, 6], [0, 65, 1, 0, 2, 3], h_local=8) == 6 + 1 + 0 + 4
-    # taper_chunk_tokens(Lsh, h) (include/taper.h): 4k prefix -> 1024 at h <= 2, 2048 at
-    # h = 4, 4096 at h = 8; a 24k prefix keeps 3072-token chunks at any h < 8 (probed as the
-    # chunk count of a one-slot request)
-    chunks = lambda lsh, h: T.max_chunk_slots([lsh], [0, 1], [0], h_local=h)
-    assert [chunks(4096, h) for h in (1, 2, 4, 8)] == [4, 4, 2, 1]
-    assert [chunks(24576, h) for h in (1, 4, 8)] == [8, 8, 6]
+    # a 3-request batch splits at the 1024-token floor: 5 chunks x 3 ready branches + 1 x 1
+    # + 0 x 2, plus one local item per branch with local tokens (65, 1, 2, 3 -> 4 items of
+    # <= 16 x 64 tokens)
+    assert T.max_chunk_slots([4097, 1, 0], [0, 3, 4, 6], [0, 65, 1, 0, 2, 3], h_local=8) == 15 + 1 + 0 + 4
+    # taper_chunk_tokens(Lsh, h, R) (include/taper.h): clamp(Lsh h R / 512, 1024, 4096) --
+    # C2 (R = 64, 4k prefixes): 1024 at h <= 2, 2048 at h = 4, 4096 at h = 8; C3 (R = 32) 24k
+    # prefix: 1536 at h = 1, 4096 at h >= 4; C5 (R = 256) 9k prefix: 4096 even at h = 1.
+    # Probed as the chunk count of request 0 (one slot; the others are empty).
+    def chunks(lsh, h, R=1):
+        return T.max_chunk_slots([lsh] + [0] * (R - 1), list(range(R + 1)), [0] * R, h_local=h)
+    assert [chunks(4096, h, 64) for h in (1, 2, 4, 8)] == [4, 4, 2, 1]
+    assert [chunks(24576, h, 32) for h in (1, 2, 4, 8)] == [16, 8, 6, 6]
+    assert chunks(9216, 1, 256) == 3
     assert chunks(100, 8) == 1 and chunks(1025, 1) == 2 and chunks(0, 1) == 0
     # local segments count per segment; bad CSR is an argument error
     assert T.max_chunk_slots([0], [0, 1], [1030], [1024, 6], h_local=8,
