@@ -83,17 +83,22 @@ constexpr int kPTHalf = 2 * kNarrowPT * kGroup * 128;  // hi + lo rows of kNarro
 constexpr int kPTBytes = (2 * kPTHalf > 2 * kSwapMaxW * kGroup * 128)
                              ? 2 * kPTHalf : 2 * kSwapMaxW * kGroup * 128;
 constexpr int kOffML = kOffPT + kPTBytes;  // (m, l) of the <= 128 stacked rows, 2 buffers
-// swap mode, cross-warp reductions per softmax group: max [2 parities][4 warps][kRedCols],
-// sum [4][kRedCols] (a group owns <= kSwapMaxWB 8-row blocks)
+// swap mode, cross-warp tile maxima per softmax group: [2 parities][4 warps][kRedCols] (a
+// group owns <= kSwapMaxWB 8-row blocks)
 constexpr int kRedCols = 8 * kSwapMaxWB;
-constexpr int kRedFloats = 3 * 4 * kRedCols;
+constexpr int kRedFloats = 2 * 4 * kRedCols;
 constexpr int kOffRed = kOffML + 2 * 128 * 8;
-// row mode: per-row tile maxima of the two token halves [2 parities][2 groups][128] and the
-// second group's row sums [2 O buffers][128]
+// row mode: per-row tile maxima of the two token halves [2 parities][2 groups][128]; then
+// the softmax warps' partial row sums [2 O buffers][4 slots][128 rows] (swap: slot = TMEM
+// quadrant warp, row: slot = group), summed by the epilogue
 constexpr int kOffRowRed = kOffRed + 2 * kRedFloats * 4;
-constexpr int kOffAlpha = kOffRowRed + (2 * 2 * 128 + 2 * 128) * 4;  // swap: rescale factors [8][kRedCols]
+constexpr int kOffLPart = kOffRowRed + 2 * 2 * 128 * 4;
+constexpr int kOffAlpha = kOffLPart + 2 * 4 * 128 * 4;  // swap: rescale factors [8][kRedCols]
 constexpr int kRecBytes = kItemTiles <= 32 ? 1024 : 2048;  // ItemRec slot
-constexpr int kItemRing = 8192 / kRecBytes;   // claimed-item ring (8 KB of ItemRec records)
+// claimed-item ring: the scheduler resolves one item ahead of the K producer, the softmax
+// warps hold theirs to the item's end, the MMA and epilogue warps copy the record at once --
+// three 2 KB records suffice
+constexpr int kItemRing = kRecBytes == 2048 ? 3 : 8;
 constexpr int kOffRec = kOffAlpha + 8 * kRedCols * 4;
 constexpr int kOffBar = kOffRec + kItemRing * kRecBytes;
 constexpr int kSmemUsed = kOffBar + 512;
@@ -356,7 +361,8 @@ struct SoftmaxCtx {  // per-thread constants of a softmax warp
   uint64_t *s_full, *pv_done, *vfull, *p_full_g, *o_free, *ml_full;
   float2 *xml;
   float *red_g, *alpha_s;
-  float *row_red, *row_lsum;  // row mode: [2][2][128] tile maxima, [2][128] group-1 row sums
+  float *row_red;  // row mode: [2][2][128] tile maxima
+  float *lpart;    // [2][4][128] partial row sums (item end, read by the epilogue)
   uint32_t tmem, lane_off, pt_base;
   int grp, wq, lane, warp, tid, bar_id;
   float c;
@@ -594,8 +600,9 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
     mbar_arrive(C.p_full_g + (n & 1));
     ++n;
   }
-  // row sums: this thread's partial over its 2 tokens per tile -> 16 tokens -> 4 warps
-  float *red_sum = C.red_g + 8 * kRedCols;
+  // row sums: this thread's partial over its 2 tokens per tile -> 16 tokens of its warp; the
+  // 4 warps' partials go to SMEM without a group barrier and the epilogue adds them (the
+  // slowest warp's item end then overlaps the next item's first tile)
   if constexpr (WB > 0) {
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
@@ -603,31 +610,25 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
       l_run[i] += __shfl_xor_sync(0xffffffffu, l_run[i], 8);
       l_run[i] += __shfl_xor_sync(0xffffffffu, l_run[i], 16);
     }
-    if (lane < 4) {
-#pragma unroll
-      for (int b = 0; b < WB; ++b) {
-        red_sum[wq * kRedCols + 8 * b + c0] = l_run[2 * b];
-        red_sum[wq * kRedCols + 8 * b + c0 + 1] = l_run[2 * b + 1];
-      }
-    }
-    named_bar_sync(C.bar_id, 128);
   }
-  // publish (m, l) for the epilogue; xml[ob] was consumed by epilogue item_idx-2
+  if (C.warp == 2 && lane == 0) trace_ev(*C.p, 1, 2048 + item_idx);
+  // publish (m, l) for the epilogue; xml[ob] / lpart[ob] were consumed by epilogue item_idx-2
   mbar_wait(C.o_free + ob, ((item_idx >> 1) & 1) ^ 1);
+  if (C.warp == 2 && lane == 0) trace_ev(*C.p, 2, 2048 + item_idx);
   if constexpr (WB > 0) {
-    if (wq == 0 && lane < 4) {
+    if (lane < 4) {
+      float *lp = C.lpart + (ob * 4 + wq) * 128 + 8 * blk0;
 #pragma unroll
       for (int b = 0; b < WB; ++b)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int cl = 8 * b + c0 + e;
-          const float L = red_sum[cl] + red_sum[kRedCols + cl] + red_sum[2 * kRedCols + cl] + red_sum[3 * kRedCols + cl];
-          C.xml[ob * 128 + 8 * blk0 + cl] = make_float2(m_run[2 * b + e], L);
+          lp[8 * b + c0 + e] = l_run[2 * b + e];
+          if (wq == 0) C.xml[ob * 128 + 8 * (blk0 + b) + c0 + e] = make_float2(m_run[2 * b + e], 0.f);
         }
     }
-    named_bar_sync(C.bar_id, 128);  // red_sum reused by the next item
   }
   mbar_arrive(C.ml_full + ob);
+  if (C.warp == 2 && lane == 0) trace_ev(*C.p, 3, 2048 + item_idx);
 }
 
 // Row mode: one shared item of w >= kRowMin branches (8 w <= 128 stacked rows; M = 128 when
@@ -760,13 +761,12 @@ __device__ TAPER_ROW_INLINE void softmax_item_row(const SoftmaxCtx C, const Item
     ++n;
   }
   if constexpr (!M128) l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);
-  // publish (m, l) for the epilogue; xml[ob] / row_lsum[ob] were consumed by item_idx-2
+  // publish (m, l) for the epilogue (which adds the two groups' partial sums); xml[ob] and
+  // lpart[ob] were consumed by epilogue item_idx-2
   mbar_wait(C.o_free + ob, ((item_idx >> 1) & 1) ^ 1);
-  if (warp_live) {
-    float *lsum = C.row_lsum + ob * 128;
-    if (grp == 1 && writer) lsum[row] = l_run;
-    named_bar_sync(pair_bar, 64);
-    if (grp == 0 && writer && row < n_live) C.xml[ob * 128 + row] = make_float2(m_run, l_run + lsum[row]);
+  if (warp_live && writer && row < n_live) {
+    C.lpart[(ob * 4 + grp) * 128 + row] = l_run;
+    if (grp == 0) C.xml[ob * 128 + row] = make_float2(m_run, 0.f);
   }
   mbar_arrive(C.ml_full + ob);
 }
@@ -810,6 +810,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sched_go + 1);
   ItemRec *recs = reinterpret_cast<ItemRec *>(smem + kOffRec);
   float2 *xml = reinterpret_cast<float2 *>(smem + kOffML);
+  const float *lpart = reinterpret_cast<const float *>(smem + kOffLPart);
   float *red = reinterpret_cast<float *>(smem + kOffRed);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1158,7 +1159,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     C.red_g = red + C.grp * kRedFloats;
     C.alpha_s = reinterpret_cast<float *>(smem + kOffAlpha) + (C.grp * 4 + C.wq) * kRedCols;
     C.row_red = reinterpret_cast<float *>(smem + kOffRowRed);
-    C.row_lsum = C.row_red + 2 * 2 * 128;
+    C.lpart = reinterpret_cast<float *>(smem + kOffLPart);
     uint32_t n = 0;
     bool prev_wide = true;
     for (uint32_t item_idx = 0;; ++item_idx) {
@@ -1170,6 +1171,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const ItemRec *rec = recs + item_idx % kItemRing;
       Item x;
       decode_item(rec, x);
+      if (warp == 2 && lane == 0) trace_ev(p, 0, 2048 + item_idx);
       if (kRowSm && x.row) {
         // (M = 64 row items exist only when kRowMin <= 8; n_r >= 9 means M = 128)
         if (kRowMin > 8 || x.m128) softmax_item_row<true>(C, x, item_idx, n);
@@ -1224,7 +1226,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         if ((m128 ? 32 * wq : 16 * wq) < 8 * x.w) {
           const bool live = row < 8 * x.w;
           const size_t prow = ((size_t)(x.cs0 + (row >> 3)) * h + x.g) * kGroup + (row & 7);
-          const float2 ml = live ? xml[ob * 128 + row] : make_float2(0.f, 0.f);
+          const float *lp = lpart + ob * 512 + row;
+          const float2 ml = live ? make_float2(xml[ob * 128 + row].x, lp[0] + lp[128]) : make_float2(0.f, 0.f);
           const float inv = ml.y > 0.f ? 1.f / ml.y : 0.f;
           float4 *dst = reinterpret_cast<float4 *>(p.part_o + prow * kHeadDim + 64 * hf);
 #pragma unroll 1
@@ -1249,16 +1252,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tmem_ld16(tO + 16 * b, o);
         tmem_ld_wait();
         const size_t prow0 = ((size_t)(x.cs0 + b) * h + x.g) * kGroup;
+        const float *lp = lpart + ob * 512 + 8 * b;  // the 4 quadrant warps' partial sums
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float2 ml = xml[ob * 128 + 8 * b + e];
-          const float inv = ml.y > 0.f ? 1.f / ml.y : 0.f;
+          const float L = (lp[e] + lp[128 + e]) + (lp[256 + e] + lp[384 + e]);
+          const float inv = L > 0.f ? 1.f / L : 0.f;
           p.part_o[(prow0 + e) * kHeadDim + d] = (__uint_as_float(o[e]) + __uint_as_float(o[8 + e])) * inv;
         }
         if (etid < 8) {
-          const float2 ml = xml[ob * 128 + 8 * b + etid];
+          const float L = (lp[etid] + lp[128 + etid]) + (lp[256 + etid] + lp[384 + etid]);
           p.part_lse[prow0 + etid] =
-              ml.y > 0.f ? (ml.x + __log2f(ml.y)) * 0.69314718055994531f : -INFINITY;
+              L > 0.f ? (xml[ob * 128 + 8 * b + etid].x + __log2f(L)) * 0.69314718055994531f : -INFINITY;
         }
       }
       // hand O^T / (m, l) back, then publish the item: the barrier orders every epilogue

@@ -80,6 +80,14 @@ def main():
         print(f"{name:18s} median {np.median(dd[ok]):8.0f} mean {dd[ok].mean():8.0f}")
     full = tr.view(cap, 16).cpu().numpy().astype(np.int64)
     ep = np.where(full[2048:2048 + 40] > 0, full[2048:2048 + 40] - t0, -1)
+    it = full[2048:2048 + 12].astype(np.int64)
+    rel = lambda v: int(v - t0) if v > 0 else -1
+    print("per item (cycles rel.): sm_start sm_rowsum sm_ofree sm_mlarrive ep_start ep_end | w nt local")
+    for i in range(12):
+        r = it[i]
+        if r[0] <= 0:
+            break
+        print(i, [rel(r[e]) for e in (0, 1, 2, 3, 10, 11)], "|", int(r[13]), int(r[14]), int(r[15]))
     print("epilogue per item: ofull->ml, ml->xdone, xdone->bar, bar->stores(w8), stores->end")
     for i in range(12):
         r = ep[i]
