@@ -70,6 +70,10 @@ def parse():
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as one CUDA graph (auto: on when G > 1 or --rank-of, "
                          "where a layer is short enough for host launch overhead to matter)")
+    ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
+                    help="G > 1: per-layer output exchange -- fused (the merge epilogue stores "
+                         "rows into every rank's buffer over NVLink, CUDA IPC; NEXT-4) or a "
+                         "NCCL all-gather on a side stream")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -337,6 +341,24 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     comm = torch.cuda.Stream(dev) if G > 1 else None  # per-layer all-gathers ride here
     launches = [0]
+    # fused gather (NEXT-4): per-layer gathered buffers + flag arrays, mapped into every rank
+    pg, gather_note = None, "nccl all_gather_into_tensor per layer on a side stream"
+    if G > 1 and args.gather == "fused":
+        ok = torch.zeros(1, device=dev)
+        try:
+            pg = par.PeerGather(S, G, rank, n_buf=L, n_flag=L, device=dev)
+        except Exception as e:  # e.g. no CUDA IPC: every rank falls back together
+            print(f"rank {rank}: fused gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
+            ok.fill_(1)
+        dist.all_reduce(ok)
+        if float(ok.item()) > 0:
+            if pg is not None:
+                pg.close()
+            pg = None
+            gather_note = "nccl all_gather (fused gather setup failed on some rank)"
+        else:
+            gather_note = ("fused: merge epilogue stores every row into all ranks' [S,64,128] "
+                           "buffers (CUDA IPC peer pointers) + per-layer flag wait")
 
     every = min(PROF_EVERY, L)
 
@@ -363,15 +385,22 @@ def run_ours(args):
             sampled = prof is not None and l % every == every - 1
             if sampled:
                 T.taper_set_profile_events(prof[l // every])
-            T.taper_decode_attention(db, adm, kvs[l], qs_[l], outs_[l], None, scale, ws)
+            if pg is not None:
+                gl = pg.gather(l, l)
+                T.taper_decode_attention_gather(db, adm, kvs[l], qs_[l], gl, None, scale, ws)
+            else:
+                T.taper_decode_attention(db, adm, kvs[l], qs_[l], outs_[l], None, scale, ws)
             if sampled:
                 T.taper_set_profile_events(None)
             n += T.taper_last_launch_count()
-            if G > 1:
+            if pg is not None:
+                T.taper_gather_wait(gl)  # the layer's consumer would run after this
+                n += T.taper_last_launch_count()
+            elif G > 1:
                 comm.wait_stream(cur)
                 with torch.cuda.stream(comm):
                     par.gather_outputs(outs_[l], gathered_[l])
-        if G > 1:
+        if G > 1 and pg is None:
             cur.wait_stream(comm)
         launches[0] = n
 
@@ -475,7 +504,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, T, torch, dist, G, batch, db, adm, ws, kvs, L, S, h, scale, dev,
-                      rank, local, step)
+                      rank, local, step, pg)
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
@@ -504,6 +533,7 @@ def run_ours(args):
                                 "no collectives; value = that rank's steps/s)"),
                 "l2": f"inputs larger than L2 ({layer_bytes / 1e9:.2f} GB K/V per layer per GPU)",
                 "step": f"admit + {L} x decode_attention (+ bcast/all-gather when G>1); no FFN",
+                "gather": gather_note if G > 1 else None,
                 "launch": ("one CUDA graph per step (kernel times from an eager profiled pass of "
                            "the same step after the timed region)" if graph is not None else
                            "eager launches; kernel times event-bracketed inside the timed region"),
@@ -534,11 +564,13 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if G > 1:
         _barrier(dist, local)
+        if pg is not None:
+            pg.close()
         dist.destroy_process_group()
 
 
 def run_e2e(args, T, torch, dist, G, batch, db, adm, ws, kvs, L, S, h, scale, dev, rank, local,
-            step_fn):
+            step_fn, pg=None):
     """Same metric through the public API with HOST buffers: every step copies the batch
     state and all layers' q from pinned host memory (copy stream, per-layer events) and
     reads back every layer's output and the admission (second copy stream), overlapped
@@ -587,17 +619,25 @@ def run_e2e(args, T, torch, dist, G, batch, db, adm, ws, kvs, L, S, h, scale, de
                 T.taper_build_work(db, adm, h, ws)
         for l in range(L):
             comp.wait_event(q_ready[l])
-            T.taper_decode_attention(db, adm, kvs[l], dq[l], dout[l], None, scale, ws)
-            if G > 1:
-                par.gather_outputs(dout[l], gathered_e2e[l])
+            if pg is not None:
+                T.taper_decode_attention_gather(db, adm, kvs[l], dq[l], pg.gather(l, l), None,
+                                                scale, ws)
+                T.taper_gather_wait(pg.gather(l, l))
+            else:
+                T.taper_decode_attention(db, adm, kvs[l], dq[l], dout[l], None, scale, ws)
+                if G > 1:
+                    par.gather_outputs(dout[l], gathered_e2e[l])
             o_ready[l].record(comp)
         with torch.cuda.stream(d2h):
             d2h.wait_event(o_ready[0])
             host_adm.copy_(adm.slot_admitted[:S], non_blocking=True)
             for l in range(L):
                 d2h.wait_event(o_ready[l])
-                host_out[l].copy_(gathered_e2e[l] if G > 1 else dout[l].unsqueeze(0),
-                                  non_blocking=True)
+                if pg is not None:
+                    host_out[l].view(S, G * 8 * h, 128).copy_(pg.out(l), non_blocking=True)
+                else:
+                    host_out[l].copy_(gathered_e2e[l] if G > 1 else dout[l].unsqueeze(0),
+                                      non_blocking=True)
         comp.wait_stream(d2h)
         comp.wait_stream(h2d)
 

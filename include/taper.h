@@ -260,6 +260,50 @@ TAPER_API int taper_decode_attention(const taper_batch *batch, const taper_admis
                            float scale, void *workspace, size_t workspace_bytes,
                            void *stream);
 
+/* ------------------------------------------------------------------ fused output gather
+ * SURVEY 8(f) NEXT-4; App. D L357 (tensor parallelism over NVLink): with the KV heads
+ * split over G ranks (rank g holds heads [g h, (g+1) h), h = 8 / G), every rank needs all
+ * 64 query heads' outputs of each layer.  Instead of a separate all-gather after the layer,
+ * the merge epilogue of taper_decode_attention_gather stores each output row straight into
+ * EVERY rank's gathered buffer (NVLink peer stores), then -- once all of this rank's rows
+ * are stored -- sets flag[rank] = 1 in every rank's flag array (release, system scope).
+ * taper_gather_wait on rank j waits until its flags of all G ranks are set and clears them
+ * (acquire), so work enqueued after it reads the complete gathered output.               */
+#define TAPER_MAX_RANKS 8
+typedef struct {            /* [host] */
+  int32_t world;            /* G in {1, 2, 4, 8}; h_local of the call must be 8 / G        */
+  int32_t rank;             /* this rank, 0 <= rank < G                                     */
+  void *out[TAPER_MAX_RANKS];        /* DEVICE pointers valid in this process: rank j's
+                                        gathered output, bf16 [S][64][128] (Q head 8 h g + i
+                                        of rank g at column block 8 h g + i); out[rank] is this
+                                        rank's own (peer pointers: taper_ipc_open)          */
+  int32_t *flags[TAPER_MAX_RANKS];   /* DEVICE pointers: rank j's flag array for THIS call,
+                                        int32 [TAPER_MAX_RANKS], zero before the call; a flag
+                                        array may be reused once its taper_gather_wait has run
+                                        (e.g. one array per layer, reused every step)       */
+} taper_gather;
+
+/* taper_decode_attention whose outputs land in every rank's gathered buffer (see above)
+ * instead of a per-rank `out`; rows of non-admitted slots are not written.  Same ordering
+ * contract and errors as taper_decode_attention, plus TAPER_ERR_ARG for a gather struct
+ * that does not match kv->h_local.                                                       */
+TAPER_API int taper_decode_attention_gather(const taper_batch *batch, const taper_admission *adm,
+                                            const taper_kv *kv, const void *q,
+                                            const taper_gather *gather, float *lse, float scale,
+                                            void *workspace, size_t workspace_bytes, void *stream);
+/* Enqueue the wait for all G ranks' rows of the matching taper_decode_attention_gather call
+ * (spins on gather->flags[gather->rank], then zeroes it; a lost flag traps after ~17 s
+ * instead of hanging).  Errors: TAPER_ERR_ARG, _CUDA.                                    */
+TAPER_API int taper_gather_wait(const taper_gather *gather, void *stream);
+
+/* CUDA IPC for the gathered buffers of other processes on the node.  taper_ipc_handle
+ * writes the 64-byte cudaIpcMemHandle_t of the allocation holding dev_ptr and dev_ptr's
+ * offset in it; taper_ipc_open maps a peer's handle and returns the peer pointer
+ * (base + offset); taper_ipc_close unmaps it.  [host]                                   */
+TAPER_API int taper_ipc_handle(const void *dev_ptr, void *handle_64_bytes, size_t *offset);
+TAPER_API int taper_ipc_open(const void *handle_64_bytes, size_t offset, void **dev_ptr);
+TAPER_API int taper_ipc_close(void *dev_ptr, size_t offset);
+
 /* Append the step's new token K/V of every admitted slot to the cache (Sec. 3.1,
  * [C-att-3]: the current token is the last token of the slot's context).  Call after the
  * lengths in `batch` include the new token and before taper_decode_attention:

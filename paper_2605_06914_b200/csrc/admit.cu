@@ -681,6 +681,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     p.hdr[3] = int(p.cap_cs > 0x7fffffff ? 0x7fffffff : p.cap_cs);
     p.hdr[4] = p.h_local;
     p.hdr[8] = 0;  // dynamic work counter of the next attend_kernel
+    p.hdr[11] = 0;  // merge CTAs done (fused gather), re-armed by every gathered merge
     p.hdr[9] = 0;  // attend CTAs exited
     *p.n_adm = n_adm;
     *p.status = st;  // the caller owns the word for this step (admit and build_work alike)

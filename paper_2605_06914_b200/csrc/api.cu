@@ -1,5 +1,8 @@
 // api.cu -- host helpers of the C ABI: errors, status strings, workspace sizing.
+#include <cuda.h>
+
 #include <cstring>
+#include <mutex>
 
 #include "host_common.h"
 #include "taper_internal.cuh"
@@ -94,5 +97,55 @@ extern "C" int taper_max_chunk_slots(int32_t n_req, int32_t n_slot, const int32_
     }
   }
   *out = total;
+  return TAPER_OK;
+}
+
+// ------------------------------------------------------------------ CUDA IPC (fused gather)
+typedef CUresult (*GetRangeFn)(CUdeviceptr *, size_t *, CUdeviceptr);
+static GetRangeFn get_range_fn() {
+  static GetRangeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<GetRangeFn>(ptr);
+  });
+  return fn;
+}
+
+extern "C" int taper_ipc_handle(const void *dev_ptr, void *handle, size_t *offset) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  if (!dev_ptr || !handle || !offset) return taper::fail(TAPER_ERR_ARG, "null ipc argument");
+  GetRangeFn range = get_range_fn();
+  if (!range) return taper::fail(TAPER_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return taper::fail(TAPER_ERR_ARG, "pointer is not device memory");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base));
+  if (e != cudaSuccess) return taper::fail_cuda(e, "cudaIpcGetMemHandle");
+  std::memcpy(handle, &h, sizeof h);
+  *offset = size_t(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return TAPER_OK;
+}
+
+extern "C" int taper_ipc_open(const void *handle, size_t offset, void **dev_ptr) {
+  if (!handle || !dev_ptr) return taper::fail(TAPER_ERR_ARG, "null ipc argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  void *base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return taper::fail_cuda(e, "cudaIpcOpenMemHandle");
+  *dev_ptr = static_cast<char *>(base) + offset;
+  return TAPER_OK;
+}
+
+extern "C" int taper_ipc_close(void *dev_ptr, size_t offset) {
+  if (!dev_ptr) return taper::fail(TAPER_ERR_ARG, "null ipc pointer");
+  cudaError_t e = cudaIpcCloseMemHandle(static_cast<char *>(dev_ptr) - offset);
+  if (e != cudaSuccess) return taper::fail_cuda(e, "cudaIpcCloseMemHandle");
   return TAPER_OK;
 }

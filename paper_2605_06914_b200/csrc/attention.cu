@@ -1316,7 +1316,22 @@ struct MergeParams {
   int h_local;
   int cap_cs;       // partial capacity of this call's workspace (checked against hdr[3])
   int32_t *status;  // taper_admission.status (TAPER_STATUS_WORK_MISMATCH)
+  // fused gather (taper_decode_attention_gather): world > 0 stores every row into all
+  // world ranks' gathered buffers [S][64][128] at Q-head column head0 + 8 g + a
+  int world, rank, head0;
+  __nv_bfloat16 *gout[TAPER_MAX_RANKS];
+  int32_t *gflags[TAPER_MAX_RANKS];
+  int32_t *gcount;  // merge CTAs done (workspace hdr[11]); the last one raises the flags
 };
+
+__device__ __forceinline__ int ld_acquire_sys(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(int32_t *p, int v) {
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // Per (admitted slot, KV head): the slot's partials are 8 contiguous GQA rows (4 KB) per
 // work item, so the warp streams whole 4 KB blocks (lane: dims 4 lane .. 4 lane + 3 of all 8
@@ -1400,8 +1415,14 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) 
         __align__(8) __nv_bfloat162 o2[2];
         o2[0] = __floats2bfloat162_rn(acc[a].x * inv, acc[a].y * inv);
         o2[1] = __floats2bfloat162_rn(acc[a].z * inv, acc[a].w * inv);
-        *reinterpret_cast<uint2 *>(p.out + ((size_t)s * qheads + g * kGroup + a) * kHeadDim + 4 * lane) =
-            *reinterpret_cast<uint2 *>(o2);
+        if (p.world == 0) {
+          *reinterpret_cast<uint2 *>(p.out + ((size_t)s * qheads + g * kGroup + a) * kHeadDim + 4 * lane) =
+              *reinterpret_cast<uint2 *>(o2);
+        } else {  // fused gather: the row goes to every rank's buffer (NVLink peer stores)
+          const size_t off = ((size_t)s * (kGroup * kGroup) + p.head0 + g * kGroup + a) * kHeadDim + 4 * lane;
+          for (int j = 0; j < p.world; ++j)
+            *reinterpret_cast<uint2 *>(p.gout[j] + off) = *reinterpret_cast<uint2 *>(o2);
+        }
         if (p.lse_out && lane == a)
           p.lse_out[(size_t)s * qheads + g * kGroup + a] = (M[a] + __log2f(Z[a])) * 0.69314718055994531f;
       }
@@ -1413,6 +1434,17 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) 
       }
     }
   }
+  if (p.world > 0) {
+    // every row of this CTA is stored (system-scope fence by each thread), then the last CTA
+    // to finish raises this rank's flag in every rank's flag array (release, system scope)
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(p.gcount, 1) == int(gridDim.x) - 1) {
+      __threadfence_system();
+      for (int j = 0; j < p.world; ++j) st_release_sys(p.gflags[j] + p.rank, 1);
+      *p.gcount = 0;  // re-armed before this kernel completes (the next merge waits for it)
+    }
+  }
   pdl_wait();  // complete only after attend_kernel (its counter re-arm) has completed
   if (tr) {
     __syncwarp();
@@ -1420,6 +1452,21 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) 
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
     p.trace[(size_t)(3200 + blockIdx.x) * 16 + 1] = (long long)g;
   }
+}
+
+// taper_gather_wait: one thread per rank polls this rank's flag of that rank (acquire,
+// system scope), then the flags are cleared for the array's next use.
+__global__ void __launch_bounds__(32, 1) gather_wait_kernel(int32_t *flags, int world) {
+  const int j = threadIdx.x;
+  if (j < world && ld_acquire_sys(flags + j) == 0) {
+    const long long t0 = clock64();
+    while (ld_acquire_sys(flags + j) == 0) {
+      __nanosleep(128);
+      if (clock64() - t0 > (1ll << 35)) __trap();  // a lost flag traps, never hangs
+    }
+  }
+  __syncwarp();
+  if (j < world) flags[j] = 0;
 }
 
 }  // namespace taper
@@ -1520,10 +1567,22 @@ static int device_sms() {
   return sms;
 }
 
-extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admission *adm,
-                                      const taper_kv *kv, const void *q, void *out, float *lse,
-                                      float scale, void *workspace, size_t workspace_bytes,
-                                      void *stream) {
+static int decode_attention(const taper_batch *batch, const taper_admission *adm,
+                            const taper_kv *kv, const void *q, void *out, const taper_gather *gather,
+                            float *lse, float scale, void *workspace, size_t workspace_bytes,
+                            void *stream) {
+  if (gather) {
+    const int G = gather->world;
+    if (!(G == 1 || G == 2 || G == 4 || G == 8) || gather->rank < 0 || gather->rank >= G)
+      return fail(TAPER_ERR_ARG, "gather: world must be 1, 2, 4 or 8 and 0 <= rank < world");
+    if (!kv || kv->h_local * G != 8) return fail(TAPER_ERR_ARG, "gather: kv->h_local must be 8 / world");
+    for (int j = 0; j < G; ++j) {
+      if (!gather->out[j] || !gather->flags[j]) return fail(TAPER_ERR_ARG, "gather: null out / flags");
+      if (reinterpret_cast<uintptr_t>(gather->out[j]) & 15)
+        return fail(TAPER_ERR_ARG, "gather: out buffers must be 16-byte aligned");
+    }
+    out = gather->out[gather->rank];
+  }
   if (!batch || !adm || !kv || !q || !out || !workspace)
     return fail(TAPER_ERR_ARG, "null argument");
   const int R = batch->n_req, S = batch->n_slot;
@@ -1622,6 +1681,14 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   mp.h_local = h;
   mp.cap_cs = ap.cap_cs;
   mp.status = adm->status;
+  mp.world = gather ? gather->world : 0;
+  mp.rank = gather ? gather->rank : 0;
+  mp.head0 = gather ? kGroup * h * gather->rank : 0;
+  for (int j = 0; j < TAPER_MAX_RANKS; ++j) {
+    mp.gout[j] = gather && j < gather->world ? static_cast<__nv_bfloat16 *>(gather->out[j]) : nullptr;
+    mp.gflags[j] = gather && j < gather->world ? gather->flags[j] : nullptr;
+  }
+  mp.gcount = ap.hdr + 11;
   const int grid = S > 0 ? S : 1;  // CTAs beyond the admitted count exit at once
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kMergeThreads);
@@ -1631,5 +1698,34 @@ extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admi
   if (e != cudaSuccess) return fail_cuda(e, "merge_kernel launch");
   if (g_prof_ev[2]) cudaEventRecord(g_prof_ev[2], st);
   set_launches(2);
+  return TAPER_OK;
+}
+
+extern "C" int taper_decode_attention(const taper_batch *batch, const taper_admission *adm,
+                                      const taper_kv *kv, const void *q, void *out, float *lse,
+                                      float scale, void *workspace, size_t workspace_bytes,
+                                      void *stream) {
+  return decode_attention(batch, adm, kv, q, out, nullptr, lse, scale, workspace, workspace_bytes,
+                          stream);
+}
+
+extern "C" int taper_decode_attention_gather(const taper_batch *batch, const taper_admission *adm,
+                                             const taper_kv *kv, const void *q,
+                                             const taper_gather *gather, float *lse, float scale,
+                                             void *workspace, size_t workspace_bytes, void *stream) {
+  if (!gather) return fail(TAPER_ERR_ARG, "null gather");
+  return decode_attention(batch, adm, kv, q, nullptr, gather, lse, scale, workspace, workspace_bytes,
+                          stream);
+}
+
+extern "C" int taper_gather_wait(const taper_gather *gather, void *stream) {
+  if (!gather || gather->world < 1 || gather->world > TAPER_MAX_RANKS || gather->rank < 0 ||
+      gather->rank >= gather->world || !gather->flags[gather->rank])
+    return fail(TAPER_ERR_ARG, "bad gather struct");
+  gather_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(gather->flags[gather->rank],
+                                                                       gather->world);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail_cuda(e, "gather_wait_kernel launch");
+  set_launches(1);
   return TAPER_OK;
 }

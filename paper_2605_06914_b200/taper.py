@@ -27,7 +27,10 @@ TAPER_CHUNK_TOKENS = 4096
 EXPORTS = ("taper_workspace_size", "taper_max_chunk_slots", "taper_admit", "taper_build_work", "taper_decode_attention",
            "taper_append_kv",
            "taper_status_string", "taper_last_error", "taper_last_launch_count",
-           "taper_set_profile_events", "taper_set_trace_buffer")
+           "taper_set_profile_events", "taper_set_trace_buffer",
+           "taper_decode_attention_gather", "taper_gather_wait", "taper_ipc_handle",
+           "taper_ipc_open", "taper_ipc_close")
+TAPER_MAX_RANKS = 8
 
 _vp = ctypes.c_void_p
 
@@ -63,6 +66,11 @@ class _KV(ctypes.Structure):
                 ("slot_pages", _vp), ("seg_page_off", _vp)]
 
 
+class _Gather(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("out", _vp * TAPER_MAX_RANKS), ("flags", _vp * TAPER_MAX_RANKS)]
+
+
 def load_library() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise RuntimeError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; "
@@ -80,6 +88,12 @@ def load_library() -> ctypes.CDLL:
                                      ctypes.c_size_t, _vp]
     lib.taper_decode_attention.argtypes = [P(_Batch), P(_Admission), P(_KV), _vp, _vp, _vp,
                                            ctypes.c_float, _vp, ctypes.c_size_t, _vp]
+    lib.taper_decode_attention_gather.argtypes = [P(_Batch), P(_Admission), P(_KV), _vp, P(_Gather),
+                                                  _vp, ctypes.c_float, _vp, ctypes.c_size_t, _vp]
+    lib.taper_gather_wait.argtypes = [P(_Gather), _vp]
+    lib.taper_ipc_handle.argtypes = [_vp, _vp, P(ctypes.c_size_t)]
+    lib.taper_ipc_open.argtypes = [_vp, ctypes.c_size_t, P(_vp)]
+    lib.taper_ipc_close.argtypes = [_vp, ctypes.c_size_t]
     lib.taper_append_kv.argtypes = [P(_Batch), P(_Admission), P(_KV), _vp, _vp, _vp]
     lib.taper_append_kv.restype = ctypes.c_int
     lib.taper_status_string.restype = ctypes.c_char_p
@@ -91,7 +105,8 @@ def load_library() -> ctypes.CDLL:
     lib.taper_set_profile_events.restype = ctypes.c_int
     lib.taper_set_profile_events.argtypes = [_vp, ctypes.c_int]
     for name in ("taper_workspace_size", "taper_admit", "taper_build_work",
-                 "taper_decode_attention"):
+                 "taper_decode_attention", "taper_decode_attention_gather", "taper_gather_wait",
+                 "taper_ipc_handle", "taper_ipc_open", "taper_ipc_close"):
         getattr(lib, name).restype = ctypes.c_int
     return lib
 
@@ -296,6 +311,59 @@ def taper_decode_attention(batch: DeviceBatch, adm: DeviceAdmission, kv: DeviceK
                                        _ptr(workspace),
                                        workspace.numel() * workspace.element_size(),
                                        _stream(stream)), "taper_decode_attention")
+
+
+class Gather:
+    """taper_gather (include/taper.h): this rank's view of the G ranks' gathered output
+    buffers ([S, 64, 128] bf16 device pointers usable in this process) and of the flag
+    arrays of one call.  Pointers only; the owner keeps the memory alive."""
+
+    def __init__(self, world: int, rank: int, outs: list[int], flags: list[int]):
+        assert len(outs) == world and len(flags) == world
+        self.world, self.rank = world, rank
+        self._c = _Gather(world, rank, (_vp * TAPER_MAX_RANKS)(*outs),
+                          (_vp * TAPER_MAX_RANKS)(*flags))
+
+    def c(self) -> _Gather:
+        return self._c
+
+
+def taper_decode_attention_gather(batch: DeviceBatch, adm: DeviceAdmission, kv: DeviceKV,
+                                  q: torch.Tensor, gather: Gather, lse: torch.Tensor | None,
+                                  scale: float, workspace: torch.Tensor, stream=None):
+    """Attention whose merge epilogue stores every output row into all ranks' gathered
+    buffers and then raises this rank's flag in every rank's flag array."""
+    assert q.dtype == torch.bfloat16 and q.is_contiguous()
+    bc, ac, kc, gc = batch.c(), adm.c(), kv.c(), gather.c()
+    _check(_lib.taper_decode_attention_gather(ctypes.byref(bc), ctypes.byref(ac), ctypes.byref(kc),
+                                              _ptr(q), ctypes.byref(gc), _ptr(lse), float(scale),
+                                              _ptr(workspace),
+                                              workspace.numel() * workspace.element_size(),
+                                              _stream(stream)), "taper_decode_attention_gather")
+
+
+def taper_gather_wait(gather: Gather, stream=None):
+    gc = gather.c()
+    _check(_lib.taper_gather_wait(ctypes.byref(gc), _stream(stream)), "taper_gather_wait")
+
+
+def taper_ipc_handle(t: torch.Tensor) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding t, t's offset in it)."""
+    buf = ctypes.create_string_buffer(64)
+    off = ctypes.c_size_t(0)
+    _check(_lib.taper_ipc_handle(_ptr(t), buf, ctypes.byref(off)), "taper_ipc_handle")
+    return buf.raw, int(off.value)
+
+
+def taper_ipc_open(handle: bytes, offset: int) -> int:
+    ptr = _vp()
+    _check(_lib.taper_ipc_open(ctypes.create_string_buffer(handle, 64), offset, ctypes.byref(ptr)),
+           "taper_ipc_open")
+    return int(ptr.value)
+
+
+def taper_ipc_close(ptr: int, offset: int):
+    _check(_lib.taper_ipc_close(ptr, offset), "taper_ipc_close")
 
 
 def taper_append_kv(batch: DeviceBatch, adm: DeviceAdmission, kv: DeviceKV,
