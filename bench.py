@@ -43,6 +43,9 @@ WORKLOADS = {
     "c5": "scaling sweep: 256 requests (128 serial + 128 parallel, Table-4 fanouts), prefixes "
           "log-U[1k,32k], branch-local U{1..256}, 64 layers",
     "c1": "tiny: 2 requests (1 serial, 1 with 4 branches), prefix 512, branch-local 32",
+    "c4": "trace replay: C2-shaped requests whose branches grow to U{32..512} tokens, reduce "
+          "stretches and new phases (synth.TraceReplay), per-step admission under the slack "
+          "schedule low (steps 0-399) / high (400-649) / moderate (650-999), 64 layers",
     "reduce": "reduce-step mix (NEXT-4): 48 requests (16 serial, 16 parallel with Table-4 "
               "fanouts, 16 reduce-phase attending to P+H plus 2-10 finished branches of "
               "U{32..512} tokens and z, each in its own pages), prefix 4096, 64 layers",
@@ -74,6 +77,12 @@ def parse():
                     help="G > 1: per-layer output exchange -- fused (the merge epilogue stores "
                          "rows into every rank's buffer over NVLink, CUDA IPC; NEXT-4) or a "
                          "NCCL all-gather on a side stream")
+    ap.add_argument("--c4-steps", type=int, default=1000,
+                    help="--config c4: trace length (the 400/250/350-step regime schedule)")
+    ap.add_argument("--latency-model", default="synthetic", choices=["synthetic", "b200"],
+                    help="admission's T(S): the synthetic (12, 0.03, 2e-5) the configs are "
+                         "defined with, or the cascade-aware OLS fit of this library on B200 "
+                         "(profiles/, NEXT-1; implies --ctx per_request)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -523,7 +532,7 @@ def run_ours(args):
             "config": {
                 "workload": f"{args.config}: {WORKLOADS[args.config]}",
                 "policy": args.policy, "ctx_counting": args.ctx, "rho": RHO,
-                "latency_model_ms": list(MODEL),
+                "latency_model_ms": list(MODEL), "latency_model": args.latency_model,
                 "slack_x": args.slack_x, "admitted_slots": int(adm_mask.sum()),
                 "ready_slots": S, "requests": R, "layers": L,
                 "kv_layer_buffers": n_distinct,
@@ -663,10 +672,146 @@ def run_e2e(args, T, torch, dist, G, batch, db, adm, ws, kvs, L, S, h, scale, de
                    "D2H inside the timed region, on two copy streams overlapped per layer"}
 
 
+def b200_model():
+    """The cascade-aware OLS fit of this library's step (NEXT-1): the paper's 20 x 25 grid
+    when it was measured (profiles/r2/latency_grid_b200.json), else the round-1 grid."""
+    for f in ("r2/latency_grid_b200.json", "latency_model_b200.json"):
+        try:
+            m = json.load(open(os.path.join(ROOT, "profiles", f)))["per_request"]
+            return (m["a_ms"], m["b_ms_per_seq"], m["c_ms_per_token"]), f
+        except Exception:
+            continue
+    raise RuntimeError("no B200 latency fit under profiles/")
+
+
+def run_c4(args):
+    """Config c4: a 1000-step trace replay -- every step a different batch
+    (branches grow, complete, reduce, re-fan), admitted on the device under the regime
+    schedule's slack.  A first pass drives the trace with the device admission and stages
+    every step's batch state and page tables in HBM; the timed pass replays the same steps
+    (admission recomputed -- bit-identical, deterministic -- plus 64 attention layers each)
+    with CUDA events at the regime boundaries.  steps/s per regime is the report."""
+    import torch
+    from paper_2605_06914_b200 import taper as T
+    assert int(os.environ.get("WORLD_SIZE", "1")) == 1, "c4 runs on one GPU"
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    model, ctx = MODEL, args.ctx
+    L, h, n_steps = args.layers, 8, args.c4_steps
+    trace = synth.TraceReplay(seed=args.seed)
+    rng = np.random.default_rng(args.seed + 7)
+    ws = torch.empty(T.taper_workspace_size(T.TAPER_MAX_SLOTS, T.TAPER_MAX_SLOTS, h, 1 << 15),
+                     dtype=torch.uint8, device=dev)
+    steps, max_pages = [], 1
+    for i in range(n_steps):
+        b = trace.batch(slack_min_ms=0.0)
+        db = T.DeviceBatch.from_host(b, dev)
+        adm = T.DeviceAdmission.empty(b.n_req, b.n_slot, dev)
+        T.taper_admit(db, model, "off", RHO, adm, h, ws, ctx=ctx)
+        t0 = float(adm.diag[0].item())
+        T.taper_admit(db, model, "eager", RHO, adm, h, ws, ctx=ctx)
+        set_slack(b, t0, float(adm.diag[2].item()), trace.slack_x(i))
+        db = T.DeviceBatch.from_host(b, dev)
+        T.taper_admit(db, model, args.policy, RHO, adm, h, ws, 2, ctx=ctx)
+        mask = adm.slot_admitted.cpu().numpy()[:b.n_slot].copy()
+        lay = synth.make_layout(b, synth.PAGE, rng, 1)
+        max_pages = max(max_pages, lay.num_pages)
+        steps.append((b, db, adm, T.page_tables_to_device(lay, dev), mask))
+        trace.advance(mask)
+    layer_bytes = 2 * max_pages * h * synth.PAGE * 128 * 2
+    n_pools = max(1, min(L, int(KV_BUDGET_BYTES // layer_bytes)))
+    gen = torch.Generator(device=dev).manual_seed(args.seed)
+    shape = (max_pages, h, synth.PAGE, 128)
+    pools = [(torch.randn(shape, generator=gen, device=dev, dtype=torch.bfloat16),
+              torch.randn(shape, generator=gen, device=dev, dtype=torch.bfloat16))
+             for _ in range(n_pools)]
+    S_max = max(st[0].n_slot for st in steps)
+    q = torch.randn((S_max, 8 * h, 128), generator=gen, device=dev, dtype=torch.bfloat16)
+    out = torch.empty_like(q)
+    kvs = [[T.DeviceKV(pools[l % n_pools][0], pools[l % n_pools][1], *st[3]) for l in range(L)]
+           for st in steps]
+    scale = 1.0 / math.sqrt(128)
+    n_launch = [0]
+
+    def run_step(i):
+        b, db, adm, _, _ = steps[i]
+        T.taper_admit(db, model, args.policy, RHO, adm, h, ws, 2, ctx=ctx)
+        n = T.taper_last_launch_count()
+        for l in range(L):
+            T.taper_decode_attention(db, adm, kvs[i][l], q, out, None, scale, ws)
+            n += T.taper_last_launch_count()
+        n_launch[0] += n
+
+    for i in range(min(max(3, args.warmup), n_steps)):
+        run_step(i)
+    torch.cuda.synchronize(dev)
+    bounds = [0, min(400, n_steps), min(650, n_steps), n_steps]
+    names = ["low load (steps 0-399, x ~ U[1.2, 2])", "high load (400-649, x ~ U[-0.5, 0.25])",
+             "moderate (650-999, x ~ U[0.25, 0.75])"]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in bounds]
+    sampler = ClockSampler(0)
+    n_launch[0] = 0
+    for k in range(3):
+        ev[k].record()
+        for i in range(bounds[k], bounds[k + 1]):
+            run_step(i)
+    ev[3].record()
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    for i in range(n_steps):  # the timed replay decided exactly what the first pass did
+        assert np.array_equal(steps[i][2].slot_admitted.cpu().numpy()[:steps[i][0].n_slot], steps[i][4])
+    regimes = {}
+    tot_ms = 0.0
+    for k in range(3):
+        if bounds[k + 1] <= bounds[k]:
+            continue
+        ms = ev[k].elapsed_time(ev[k + 1])
+        tot_ms += ms
+        nb = sum(algorithmic_bytes(steps[i][0], steps[i][4], h)["layer"] for i in range(bounds[k], bounds[k + 1]))
+        adm_rate = np.mean([(steps[i][4].sum() - steps[i][0].n_req) / max(1, steps[i][0].n_slot - steps[i][0].n_req)
+                            for i in range(bounds[k], bounds[k + 1])])
+        regimes[names[k]] = {"steps": bounds[k + 1] - bounds[k], "steps_per_s": (bounds[k + 1] - bounds[k]) / (ms / 1e3),
+                             "ms_per_step": ms / (bounds[k + 1] - bounds[k]),
+                             "attn_gbs": L * nb / (ms * 1e-3) / 1e9,
+                             "admitted_slots_mean": float(np.mean([steps[i][4].sum() for i in range(bounds[k], bounds[k + 1])])),
+                             "opportunistic_admission_rate": float(adm_rate)}
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    total_bytes = L * sum(algorithmic_bytes(st[0], st[4], h)["layer"] for st in steps)
+    gbs = total_bytes / (tot_ms * 1e-3) / 1e9
+    line = {"metric": METRIC, "value": n_steps / (tot_ms / 1e3), "unit": "steps/s", "n_gpus": 1,
+            "steps": n_steps, "warmup": max(3, args.warmup), "ms_per_step": tot_ms / n_steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded N(0,1) bf16 K/V/q; no model weights)",
+            "config": {"workload": f"c4: {WORKLOADS['c4']}", "policy": args.policy,
+                       "ctx_counting": ctx, "latency_model_ms": list(model), "rho": RHO,
+                       "layers": L, "kv_layer_buffers": n_pools,
+                       "step": f"admit + {L} x decode_attention per step, every step a new batch "
+                               "(state and page tables staged in HBM by an untimed first pass)",
+                       "l2": f"inputs larger than L2 ({layer_bytes / 1e9:.2f} GB K/V per layer)"},
+            "regimes": regimes,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": gbs / hbm_peak, "traffic": None,
+                         "kernel": "whole step (admit + attend + merge), algorithmic bytes"},
+            "gpu_launches": n_launch[0], "clocks": clocks,
+            "e2e": None, "cpu_baseline": None}
+    print(json.dumps(line), flush=True)
+
+
 def main():
+    global MODEL
     args = parse()
+    if args.latency_model == "b200":  # NEXT-1: admit with this library's fitted step model
+        MODEL = b200_model()[0]
+        args.ctx = "per_request"
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c4":
+        run_c4(args)
     else:
         run_ours(args)
 

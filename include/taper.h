@@ -215,6 +215,27 @@ TAPER_API int taper_max_chunk_slots(int32_t n_req, int32_t n_slot,
                                     const int32_t *seg_len, int32_t h_local,
                                     int64_t *max_chunk_slots);
 
+/* ------------------------------------------------------------------ latency model refit
+ * App. C.1 "Fitting": T(S) = a + b n + c L is fitted by ordinary least
+ * squares and "refreshed every 10 minutes using a rolling window of the most recent 200
+ * observed step latencies".  The window keeps the last TAPER_LATENCY_WINDOW observations
+ * (n = sequences in the step, L = its context count -- per sequence or per request, as the
+ * admission counts it -- and the measured step time in ms); taper_latency_refit solves the
+ * 3x3 normal equations in fp64.  The fitted model replaces *model only if it keeps T
+ * monotone (a >= 0, b > 0, c > 0; L341) and the window holds >= 3 observations with a
+ * non-singular design; otherwise *model is left as it was and TAPER_ERR_NONMONOTONE /
+ * TAPER_ERR_ARG is returned.  fit_out (optional, [3]): R^2, MAPE (fraction), RMSE (ms)
+ * of the new fit over the window.  All [host], no GPU.                                   */
+#define TAPER_LATENCY_WINDOW 200
+typedef struct {
+  int32_t count;  /* observations held (<= TAPER_LATENCY_WINDOW)  */
+  int32_t head;   /* next slot to overwrite                        */
+  double n[TAPER_LATENCY_WINDOW], L[TAPER_LATENCY_WINDOW], t_ms[TAPER_LATENCY_WINDOW];
+} taper_latency_window;
+TAPER_API int taper_latency_observe(taper_latency_window *w, double n, double L, double t_ms);
+TAPER_API int taper_latency_refit(const taper_latency_window *w, taper_latency_model *model,
+                                  double *fit_out);
+
 /* One admission step (Sec. 3.3 + Alg. 1; fixed policies of App. D), then the attention
  * work list for this rank (h_local KV heads) is written into `workspace`.
  * Greedy with linear utility is evaluated as a sort of candidates by (dL, r, slot)

@@ -1,6 +1,7 @@
 // api.cu -- host helpers of the C ABI: errors, status strings, workspace sizing.
 #include <cuda.h>
 
+#include <cmath>
 #include <cstring>
 #include <mutex>
 
@@ -147,5 +148,60 @@ extern "C" int taper_ipc_close(void *dev_ptr, size_t offset) {
   if (!dev_ptr) return taper::fail(TAPER_ERR_ARG, "null ipc pointer");
   cudaError_t e = cudaIpcCloseMemHandle(static_cast<char *>(dev_ptr) - offset);
   if (e != cudaSuccess) return taper::fail_cuda(e, "cudaIpcCloseMemHandle");
+  return TAPER_OK;
+}
+
+// ------------------------------------------------------------------ latency model refit
+extern "C" int taper_latency_observe(taper_latency_window *w, double n, double L, double t_ms) {
+  if (!w || !(n >= 0) || !(L >= 0) || !(t_ms >= 0)) return taper::fail(TAPER_ERR_ARG, "bad observation");
+  if (w->count < 0 || w->count > TAPER_LATENCY_WINDOW || w->head < 0 || w->head >= TAPER_LATENCY_WINDOW)
+    return taper::fail(TAPER_ERR_ARG, "corrupt latency window");
+  w->n[w->head] = n;
+  w->L[w->head] = L;
+  w->t_ms[w->head] = t_ms;
+  w->head = (w->head + 1) % TAPER_LATENCY_WINDOW;
+  if (w->count < TAPER_LATENCY_WINDOW) ++w->count;
+  return TAPER_OK;
+}
+
+// OLS through the normal equations X^T X beta = X^T y, X = [1, n, L], in fp64 with the
+// columns centred (the intercept is recovered afterwards) so that L ~ 1e5 does not swamp
+// the 3x3 system; Cramer's rule on the centred 2x2 block.
+extern "C" int taper_latency_refit(const taper_latency_window *w, taper_latency_model *model,
+                                   double *fit_out) {
+  if (!w || !model || w->count < 0 || w->count > TAPER_LATENCY_WINDOW)
+    return taper::fail(TAPER_ERR_ARG, "bad refit arguments");
+  const int m = w->count;
+  if (m < 3) return taper::fail(TAPER_ERR_ARG, "fewer than 3 observations");
+  double mn = 0, mL = 0, mt = 0;
+  for (int i = 0; i < m; ++i) { mn += w->n[i]; mL += w->L[i]; mt += w->t_ms[i]; }
+  mn /= m; mL /= m; mt /= m;
+  double snn = 0, sLL = 0, snL = 0, snt = 0, sLt = 0, stt = 0;
+  for (int i = 0; i < m; ++i) {
+    const double dn = w->n[i] - mn, dL = w->L[i] - mL, dt = w->t_ms[i] - mt;
+    snn += dn * dn; sLL += dL * dL; snL += dn * dL; snt += dn * dt; sLt += dL * dt; stt += dt * dt;
+  }
+  const double det = snn * sLL - snL * snL;
+  if (!(det > 1e-12 * snn * sLL) || snn <= 0 || sLL <= 0)
+    return taper::fail(TAPER_ERR_ARG, "singular design (n and L collinear or constant)");
+  const double b = (snt * sLL - sLt * snL) / det;
+  const double c = (sLt * snn - snt * snL) / det;
+  const double a = mt - b * mn - c * mL;
+  if (!(a >= 0) || !(b > 0) || !(c > 0))
+    return taper::fail(TAPER_ERR_NONMONOTONE, "refit would make T non-monotone (a < 0, b <= 0 or c <= 0)");
+  if (fit_out) {
+    double sse = 0, ape = 0;
+    for (int i = 0; i < m; ++i) {
+      const double r = w->t_ms[i] - (a + b * w->n[i] + c * w->L[i]);
+      sse += r * r;
+      ape += w->t_ms[i] > 0 ? std::fabs(r) / w->t_ms[i] : 0.0;
+    }
+    fit_out[0] = stt > 0 ? 1.0 - sse / stt : 1.0;
+    fit_out[1] = ape / m;
+    fit_out[2] = std::sqrt(sse / m);
+  }
+  model->a = a;
+  model->b = b;
+  model->c = c;
   return TAPER_OK;
 }

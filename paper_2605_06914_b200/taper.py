@@ -29,8 +29,9 @@ EXPORTS = ("taper_workspace_size", "taper_max_chunk_slots", "taper_admit", "tape
            "taper_status_string", "taper_last_error", "taper_last_launch_count",
            "taper_set_profile_events", "taper_set_trace_buffer",
            "taper_decode_attention_gather", "taper_gather_wait", "taper_ipc_handle",
-           "taper_ipc_open", "taper_ipc_close")
+           "taper_ipc_open", "taper_ipc_close", "taper_latency_observe", "taper_latency_refit")
 TAPER_MAX_RANKS = 8
+TAPER_LATENCY_WINDOW = 200
 
 _vp = ctypes.c_void_p
 
@@ -71,6 +72,13 @@ class _Gather(ctypes.Structure):
                 ("out", _vp * TAPER_MAX_RANKS), ("flags", _vp * TAPER_MAX_RANKS)]
 
 
+class _Window(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int32), ("head", ctypes.c_int32),
+                ("n", ctypes.c_double * TAPER_LATENCY_WINDOW),
+                ("L", ctypes.c_double * TAPER_LATENCY_WINDOW),
+                ("t_ms", ctypes.c_double * TAPER_LATENCY_WINDOW)]
+
+
 def load_library() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise RuntimeError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; "
@@ -94,6 +102,8 @@ def load_library() -> ctypes.CDLL:
     lib.taper_ipc_handle.argtypes = [_vp, _vp, P(ctypes.c_size_t)]
     lib.taper_ipc_open.argtypes = [_vp, ctypes.c_size_t, P(_vp)]
     lib.taper_ipc_close.argtypes = [_vp, ctypes.c_size_t]
+    lib.taper_latency_observe.argtypes = [P(_Window), ctypes.c_double, ctypes.c_double, ctypes.c_double]
+    lib.taper_latency_refit.argtypes = [P(_Window), P(_Model), P(ctypes.c_double)]
     lib.taper_append_kv.argtypes = [P(_Batch), P(_Admission), P(_KV), _vp, _vp, _vp]
     lib.taper_append_kv.restype = ctypes.c_int
     lib.taper_status_string.restype = ctypes.c_char_p
@@ -106,7 +116,8 @@ def load_library() -> ctypes.CDLL:
     lib.taper_set_profile_events.argtypes = [_vp, ctypes.c_int]
     for name in ("taper_workspace_size", "taper_admit", "taper_build_work",
                  "taper_decode_attention", "taper_decode_attention_gather", "taper_gather_wait",
-                 "taper_ipc_handle", "taper_ipc_open", "taper_ipc_close"):
+                 "taper_ipc_handle", "taper_ipc_open", "taper_ipc_close", "taper_latency_observe",
+                 "taper_latency_refit"):
         getattr(lib, name).restype = ctypes.c_int
     return lib
 
@@ -364,6 +375,31 @@ def taper_ipc_open(handle: bytes, offset: int) -> int:
 
 def taper_ipc_close(ptr: int, offset: int):
     _check(_lib.taper_ipc_close(ptr, offset), "taper_ipc_close")
+
+
+class LatencyWindow:
+    """taper_latency_window (include/taper.h): the rolling window of the last 200 observed
+    steps (App. C.1 "Fitting", L337) and its OLS refit of T(S) = a + b n + c L."""
+
+    def __init__(self):
+        self._w = _Window()
+
+    def observe(self, n: float, L: float, t_ms: float):
+        _check(_lib.taper_latency_observe(ctypes.byref(self._w), float(n), float(L), float(t_ms)),
+               "taper_latency_observe")
+
+    @property
+    def count(self) -> int:
+        return int(self._w.count)
+
+    def refit(self, model) -> tuple[tuple[float, float, float], dict]:
+        """(new model, {r2, mape, rmse_ms}); raises TaperError (the model unchanged) when the
+        fit would not be monotone or the window is degenerate."""
+        m = _Model(*model)
+        fit = (ctypes.c_double * 3)()
+        _check(_lib.taper_latency_refit(ctypes.byref(self._w), ctypes.byref(m), fit),
+               "taper_latency_refit")
+        return (m.a, m.b, m.c), {"r2": fit[0], "mape": fit[1], "rmse_ms": fit[2]}
 
 
 def taper_append_kv(batch: DeviceBatch, adm: DeviceAdmission, kv: DeviceKV,

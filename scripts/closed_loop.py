@@ -55,6 +55,7 @@ class Req:
     done: bool = False
     segs: list = None      # reduce stage: finished branches' lengths (canonical order)
     z: int = 0             # reduce tokens so far (the last local segment)
+    phase: int = 0         # parallel phases started (the no-replanning ablation commits per phase)
 
     def start_stage(self):
         while self.stages:
@@ -64,6 +65,7 @@ class Req:
                 return
             if kind == "parallel":
                 self.branches = [[1, t] for t in arg]  # the first branch token is in the cache
+                self.phase += 1
                 return
         self.done = True
 
@@ -182,9 +184,43 @@ def context_per_request(b, adm):
     return L
 
 
-def run(policy, admit_fn, step_fn, n_steps, seed=0, rho=0.8, model=None, refit=False):
+def canonical_first(b, i, w):
+    """Request i's first w ready slots in canonical order (ascending local length, then
+    slot index -- reading C-adm-1): Cap(w) for one request."""
+    off = b.req_slot_off
+    slots = np.arange(off[i], off[i + 1])
+    order = slots[np.lexsort((slots, b.slot_local_len[slots]))]
+    m = np.zeros(b.n_slot, bool)
+    m[order[:max(1, w)]] = True
+    return m
+
+
+def predict(model, b, adm):
+    """App. C.1 T(S) = a + b n + c L with the cascade-aware per-request context."""
+    return model[0] + model[1] * int(adm.sum()) + model[2] * context_per_request(b, adm)
+
+
+# Table 1 ablations (PAPER.md L217-238) on top of the product's admission:
+#   noslack : "without the slack budget" -- every request's slack is unbounded, so the
+#             planner admits every branch that fits (near Eager);
+#   noreplan: "without per-step replanning" -- a request's width is committed at the first
+#             step of each parallel phase (TAPER's decision then) and held until the reduce;
+#   const   : "with a constant latency predictor" -- every sequence costs the same, whatever
+#             its context: T = a + (b + c L_ref) n with L_ref a fixed typical context;
+#   rho     : the slack fraction sweep (taper at rho 0.5 / 1.0).
+ABLATIONS = ("noslack", "noreplan", "const")
+L_REF = 4096
+
+
+def run(policy, admit_fn, step_fn, n_steps, seed=0, rho=0.8, model=None, refit=False,
+        ablation=None, set_mask=None):
     """admit_fn(batch, policy, rho, model) -> (slot mask, predicted T(S) ms);
-    step_fn(batch, mask) -> realised step ms."""
+    step_fn(batch, mask) -> realised step ms; set_mask(batch, mask): hand a mask composed
+    outside the admission (the no-replanning ablation) to the step's work list."""
+    assert ablation in (None,) + ABLATIONS
+    if ablation == "const" and model is not None:
+        model = (model[0], model[1] + model[2] * L_REF, model[2] * 1e-9)
+    committed = {}  # no-replanning: (rid, phase) -> width
     rng = np.random.default_rng(seed)
     fit = RollingFit(model) if model is not None else None
     pred_err = []
@@ -208,7 +244,25 @@ def run(policy, admit_fn, step_fn, n_steps, seed=0, rho=0.8, model=None, refit=F
             now += 1.0
             continue
         b = batch_of(active, now)
+        if ablation == "noslack":
+            b.req_slack_ms = np.full(b.n_req, 1e12)
         adm, t_pred = admit_fn(b, policy, rho, fit.model if fit else None)
+        if ablation == "noreplan":
+            m = np.zeros(b.n_slot, bool)
+            off = b.req_slot_off
+            for i, r in enumerate(active):
+                if r.branches:
+                    key = (r.rid, r.phase)
+                    if key not in committed:
+                        committed[key] = int(adm[off[i]:off[i + 1]].sum())
+                    m |= canonical_first(b, i, committed[key])
+                else:
+                    m[off[i]:off[i + 1]] = True
+            if not np.array_equal(m, adm):
+                adm = m
+                t_pred = predict(fit.model, b, adm) if fit else t_pred
+                if set_mask is not None:
+                    set_mask(b, adm)
         t = step_fn(b, adm)
         pred_err.append((t - t_pred) / t)
         if fit is not None and refit:
@@ -239,6 +293,7 @@ def run(policy, admit_fn, step_fn, n_steps, seed=0, rho=0.8, model=None, refit=F
         "predictor_rel_err_median": float(np.median(pred_err)),
         "predictor_rel_err_p95_abs": float(np.percentile(np.abs(pred_err), 95)),
         "final_model": fit.model if fit else None,
+        "ablation": ablation,
     }
 
 
@@ -272,6 +327,10 @@ def gpu_drivers(timed_layers):
         return (adm.slot_admitted.cpu().numpy()[:b.n_slot].astype(bool),
                 float(adm.diag[2].item()))
 
+    def set_mask(b, adm_mask):
+        state["adm"].slot_admitted[:b.n_slot].copy_(torch.from_numpy(adm_mask.astype(np.uint8)))
+        T.taper_build_work(state["db"], state["adm"], 8, ws)
+
     def step_fn(b, adm_mask):
         lay = synth.make_layout(b, 64, np.random.default_rng(len(b.slot_local_len)))
         assert lay.num_pages <= pool_pages, lay.num_pages
@@ -292,7 +351,7 @@ def gpu_drivers(timed_layers):
         attn = float(np.median(blocks)) * 64 / per
         return attn + REST[0] + REST[1] * int(adm_mask.sum())
 
-    return admit_fn, step_fn, model
+    return admit_fn, step_fn, model, set_mask
 
 
 def main():
@@ -301,22 +360,30 @@ def main():
     ap.add_argument("--policies", default="off,cap2,cap5,eager,taper")
     ap.add_argument("--rhos", default="0.5,1.0", help="extra TAPER rho sweep (Table 1)")
     ap.add_argument("--timed-layers", type=int, default=24)
+    ap.add_argument("--ablations", default="noslack,noreplan,const",
+                    help="Table 1 ablations of TAPER (PAPER.md L217-238)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "closed_loop.json"))
     args = ap.parse_args()
-    admit_fn, step_fn, model = gpu_drivers(args.timed_layers)
-    runs = [(p, 0.8) for p in args.policies.split(",")]
-    runs += [("taper", float(x)) for x in args.rhos.split(",") if x]
+    admit_fn, step_fn, model, set_mask = gpu_drivers(args.timed_layers)
+    runs = [(p, 0.8, None) for p in args.policies.split(",")]
+    runs += [("taper", float(x), None) for x in args.rhos.split(",") if x]
+    runs += [("taper", 0.8, a) for a in args.ablations.split(",") if a]
     res = []
-    runs += [("taper-refit", 0.8)]  # App. C.2 rolling refresh (unstable here: see DESIGN)
-    for p, rho in runs:
+    runs += [("taper-refit", 0.8, None)]  # App. C.2 rolling refresh (unstable here: see DESIGN)
+    for p, rho, abl in runs:
         r = run(p.split("-")[0], admit_fn, step_fn, args.steps, rho=rho, model=model,
-                refit=p.endswith("-refit"))
-        r["variant"] = p
+                refit=p.endswith("-refit"), ablation=abl, set_mask=set_mask)
+        r["variant"] = p + (f"-{abl}" if abl else "")
         res.append(r)
         print(json.dumps(r), flush=True)
+    off = next(r for r in res if r["variant"] == "off")
+    table1 = {r["variant"] + (f"@rho{r['rho']}" if r["rho"] != 0.8 else ""):
+              {"goodput_over_off": r["goodput_tok_s"] / off["goodput_tok_s"],
+               "attainment": r["attainment"]} for r in res}
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
-    json.dump({"predictor_ms": model, "rest_ms": REST, "slo_ms": SLO_MS, "runs": res},
-              open(args.out, "w"), indent=1)
+    json.dump({"predictor_ms": model, "rest_ms": REST, "slo_ms": SLO_MS, "table1_analog": table1,
+               "runs": res}, open(args.out, "w"), indent=1)
+    print(json.dumps({"table1_analog": table1}), flush=True)
 
 
 if __name__ == "__main__":

@@ -65,3 +65,33 @@ def test_rolling_refit_recovers_the_step_model():
     r = CL.run("taper", admit_fn, step_fn, 400, seed=2, model=(5.0, 0.05, 1e-5), refit=True)
     np.testing.assert_allclose(r["final_model"], MODEL, rtol=1e-6)
     assert abs(r["predictor_rel_err_median"]) < 1e-6
+
+
+def test_table1_ablations_run_and_behave():
+    """Table 1 ablation switches: without the slack budget the planner
+    admits every ready branch (= Eager's admission); without per-step replanning a request's
+    width is held for its whole phase; a constant predictor prices every sequence alike."""
+    admit_fn, step_fn = _drivers()
+    res = {a: CL.run("taper", admit_fn, step_fn, 500, seed=3, model=MODEL, ablation=a)
+           for a in CL.ABLATIONS}
+    eager = CL.run("eager", admit_fn, step_fn, 500, seed=3, model=MODEL)
+    assert res["noslack"]["admission_rate"] == 1.0
+    assert res["noslack"]["throughput_tok_s"] == pytest.approx(eager["throughput_tok_s"])
+    for r in res.values():
+        assert 0.0 <= r["attainment"] <= 1.0 and r["finished"] > 20
+    taper = CL.run("taper", admit_fn, step_fn, 500, seed=3, model=MODEL)
+    # a phase's first step admits its fresh branches (Lloc = 1, the cheapest candidates), and
+    # without replanning that width is held while the load builds: the controller cannot
+    # contract mid-phase (the paper's failure mode at load transitions)
+    assert res["noreplan"]["admission_rate"] >= taper["admission_rate"]
+    assert res["noreplan"]["attainment"] <= taper["attainment"]
+    assert 0.0 < res["const"]["admission_rate"] < 1.0
+
+
+def test_canonical_first_is_cap_per_request():
+    import synth
+    b = synth.make_batch([100, 50], [3, 2], [7, 2, 9, 4, 4], 1e3, 0.0)
+    m = CL.canonical_first(b, 0, 2)
+    assert m.tolist() == [True, True, False, False, False]  # local 7, 2, 9 -> slots 1, 0
+    m = CL.canonical_first(b, 1, 1)
+    assert m.tolist() == [False, False, False, True, False]  # tie 4, 4 -> lower slot
