@@ -505,6 +505,12 @@ def run_ours(args):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    read_ceiling = None  # TMA read-only probe of 16 KB page tiles (profiles/r2/hbm_read_ceiling.json)
+    try:
+        read_ceiling = float(json.load(open(os.path.join(ROOT, "profiles", "r2", "hbm_read_ceiling.json")))[
+            "read_only_ceiling_gbs"])
+    except Exception:
+        pass
     sh_gbs = by["attend_kernel"] / (sh_avg * 1e-3) / 1e9
     attn_gbs = by["layer"] / (layer_ms * 1e-3) / 1e9
     step_gbs = G * L * by["layer"] / (ms_per_step * 1e-3) / 1e9  # whole job, all ranks
@@ -564,7 +570,9 @@ def run_ours(args):
                          if traffic else None,
                          "kernel": "attend_kernel",
                          "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                         "bytes_per_launch": by["attend_kernel"]},
+                         "bytes_per_launch": by["attend_kernel"],
+                         "read_only_ceiling_gbs": read_ceiling,
+                         "frac_of_read_only_ceiling": sh_gbs / read_ceiling if read_ceiling else None},
             "gpu_launches": launches[0] * args.steps,
             "clocks": clocks,
             "e2e": e2e,

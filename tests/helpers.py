@@ -75,11 +75,22 @@ class Case:
                                 self.scale, b.slot_seg_off, b.seg_len, lay.seg_page_off)
 
 
+# C-att-5 diagnostics of every comparison (max abs error, max relative error over |r| >= 1e-3,
+# worst bound use), written by tests/conftest.py to gpurun_out/parity_diagnostics.json
+DIAGNOSTICS: list[dict] = []
+
+
 def assert_close(gpu: np.ndarray, ref: np.ndarray, what=""):
     """Pass iff every element satisfies |x - r| <= 2e-3 + 1e-2 |r| [C-att-5]."""
     gpu = np.asarray(gpu, np.float64)
     err = np.abs(gpu - ref)
     bound = TOL_ABS + TOL_REL * np.abs(ref)
+    big = np.abs(ref) >= 1e-3
+    DIAGNOSTICS.append({
+        "what": what, "elements": int(err.size),
+        "max_abs": float(np.nanmax(err)) if err.size else 0.0,
+        "max_rel": float(np.nanmax(err[big] / np.abs(ref[big]))) if big.any() else 0.0,
+        "max_bound_use": float(np.nanmax(err / bound)) if err.size else 0.0})
     bad = ~(err <= bound)
     if bad.any():
         i = np.argwhere(bad)[0]
