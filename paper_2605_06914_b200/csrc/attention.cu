@@ -161,6 +161,21 @@ struct AttnParams {
 #endif
 constexpr bool kTrace = TAPER_TRACE;
 __device__ __forceinline__ bool tracing(const AttnParams &p) { return kTrace && p.trace != nullptr; }
+__device__ __forceinline__ void trace_cta(const AttnParams &p, int e) {  // globaltimer, CTA row
+  if (tracing(p)) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    p.trace[(size_t)(3000 + blockIdx.x) * 16 + e] = (long long)g;
+  }
+}
+// as trace_cta, but the timestamp is taken once `dep` is available (waits for its load)
+__device__ __forceinline__ void trace_cta_dep(const AttnParams &p, int e, int dep) {
+  if (tracing(p)) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g) : "r"(dep) : "memory");
+    p.trace[(size_t)(3000 + blockIdx.x) * 16 + e] = (long long)g + (dep == 0x7fffffff);
+  }
+}
 __device__ __forceinline__ void trace_ev(const AttnParams &p, int e, uint32_t n) {
   if (tracing(p) && blockIdx.x == 0 && int(n) < p.trace_cap)
     p.trace[(size_t)n * 16 + e] = clock64();
@@ -861,6 +876,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tid == 0) trace_cta(p, 5);  // prologue done
   // PDL: the prologue above overlapped the previous kernel; wait for its memory, then let
   // the merge kernel launch (it reads the work list, which is complete and visible once
   // this grid's dependency has resolved; its warps then wait for per-request completion
@@ -883,20 +899,31 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // the kernel still draining in front of this one, the epoch moves before the re-check
     // below and the first item is resolved again (include/taper.h ordering contract).
     int epoch = kEarlyClaim ? ld_acquire(p.hdr + kHdrEpoch) : 0;
+    if (lane == 0) trace_cta_dep(p, 11, epoch);  // epoch (acquire) loaded
     // items per KV head, or none if the work list was written for another workspace / h
     auto count_items = [&]() {
       const bool ok = __ldcg(p.hdr + 4) == h && __ldcg(p.hdr + 3) == p.cap_cs;
       return ok ? (__ldcg(p.hdr) + __ldcg(p.hdr + 5)) * h : 0;
     };
     int n_items = count_items();
+    if (lane == 0) trace_cta_dep(p, 12, n_items);  // header loaded
     int *work_counter = p.hdr + 8;
-    // claim index `it` -> the SMEM record (descriptor, per-tile geometry and pages)
-    auto resolve = [&](ItemRec *rec, int it, int &w, int &adm_off, int &g) {
-      w = 0; adm_off = 0; g = 0;
+    // the descriptor of claim index `it` (longest first, then KV head), loaded before the
+    // claim is known to be valid (the index is clamped into the table) so that its latency
+    // overlaps the header loads: one dependent global load less on the way to the first TMA
+    auto load_desc = [&](int it) -> int32_t {
+      int qi = (it > 0 ? it : 0) / h;
+      qi = qi < p.cap_cs - 1 ? qi : (p.cap_cs > 0 ? p.cap_cs - 1 : 0);
+      return lane < 8 ? __ldcg(reinterpret_cast<const int32_t *>(p.sorted + qi) + lane) : 0;
+    };
+    // claim index `it` (-1: none) -> the SMEM record (descriptor, per-tile geometry and
+    // pages); slot_j = the admitted slot of the item's branch `lane` (its Q rows), loaded
+    // alongside the pages
+    auto resolve = [&](ItemRec *rec, int it, int32_t d, int &w, int &adm_off, int &g, int &slot_j) {
+      w = 0; adm_off = 0; g = 0; slot_j = 0;
       if (it >= 0) {
-        const int qi = it / h;  // claim index -> descriptor (longest first), then KV head
+        const int qi = it / h;
         g = it - qi * h;
-        const int32_t d = lane < 8 ? __ldcg(reinterpret_cast<const int32_t *>(p.sorted + qi) + lane) : 0;
         const int nt = __shfl_sync(0xffffffffu, d, 6);
         Item x;
         x.r = __shfl_sync(0xffffffffu, d, 0);
@@ -906,6 +933,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         x.te = __shfl_sync(0xffffffffu, d, 5);
         x.local = __shfl_sync(0xffffffffu, d, 7) & kItemLocal;
         if (lane < 8) rec->desc[lane] = d;
+        if (lane < w) slot_j = __ldcg(p.adm_by_req + adm_off + lane);
         for (int t = lane; t < nt; t += 32) {
           const TileInfo ti = tile_info(p, x, t);
           rec->tok0[t] = ti.tok0;
@@ -926,12 +954,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         it = (kEarlyClaim && k == 0) ? int(blockIdx.x)
                                      : (kEarlyClaim ? int(gridDim.x) : 0) + atomicAdd(work_counter, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
+      int32_t d = load_desc(it);
+      if (k == 0 && lane == 0) trace_cta_dep(p, 13, d);  // descriptor loaded
       const uint32_t slot = k % kItemRing;
       ItemRec *rec = recs + slot;
       mbar_wait(it_empty + slot, ((k / kItemRing) & 1) ^ 1);
-      int w, adm_off, g;
+      int w, adm_off, g, slot_j;
       for (bool early = kEarlyClaim && k == 0;;) {
-        resolve(rec, it < n_items ? it : -1, w, adm_off, g);
+        resolve(rec, it < n_items ? it : -1, d, w, adm_off, g, slot_j);
+        if (k == 0 && lane == 0) trace_cta(p, early ? 6 : 7);  // first record resolved
         if (!early) break;
         // The first record was resolved while the previous kernel drained.  Now wait for
         // it (q, the K/V pools and a just-written work list become visible), let the merge
@@ -939,8 +970,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         early = false;
         pdl_wait();
         pdl_launch_dependents();
+        if (lane == 0) trace_cta(p, 8);  // grid dependency resolved
         if (ld_acquire(p.hdr + kHdrEpoch) == epoch) break;
         n_items = count_items();
+        d = load_desc(it);
         __syncwarp();
       }
       if (it >= n_items) it = -1;
@@ -951,12 +984,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       // (d-lo, GQA row, d-half, slot * h + g) -> [d-half][8 rows][128 B] per branch
       const uint32_t qb = k & 1;
       mbar_wait(q_free + qb, ((k >> 1) & 1) ^ 1);
-      const int slot_j = lane < w ? __ldg(p.adm_by_req + adm_off + lane) : 0;
       if (elect_one()) mbar_arrive_expect_tx(q_full + qb, w * 2048);
       __syncwarp();
       if (lane < w)
         tma_load_4d(smem + kOffQ + qb * kQBytes + lane * 2048, &tmQ, q_full + qb, 0, 0, 0,
                     slot_j * h + g);
+      if (k == 0 && lane == 0) trace_cta(p, 9);  // first Q load issued
       __syncwarp();
     }
   } else if (warp == 0 || warp == 10) {
@@ -1065,6 +1098,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t tO = tmem_u + kColO + ob * 128;
       mbar_wait(q_full + qb, (item_idx >> 1) & 1);
       if (lane == 0) trace_ev(p, 6, n);
+      if (item_idx == 0 && lane == 0) trace_cta(p, 10);  // first Q landed
       tc_fence_after();
       // One tile loop per mode (selected once per item): a per-tile mode branch in this
       // latency-critical loop slowed swap-only layers by ~1.7 % (r2 run m).

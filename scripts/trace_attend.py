@@ -54,6 +54,13 @@ def main():
     print("per-CTA (us): start min/max %.1f/%.1f, first TMA median %.1f, end min/median/max %.1f/%.1f/%.1f" % (
         (cta[:, 0].min() - g0) / 1e3, (cta[:, 0].max() - g0) / 1e3, np.median(cta[:, 2] - g0) / 1e3,
         (cta[:, 1].min() - g0) / 1e3, np.median(cta[:, 1] - g0) / 1e3, (cta[:, 1].max() - g0) / 1e3))
+    ctaf = tr.view(cap, 16).cpu().numpy()[3000:3000 + 148].astype(np.int64)
+    for e, name in ((5, "prologue done"), (11, "epoch loaded (acquire)"), (12, "header loaded"),
+                    (13, "first descriptor loaded"), (6, "first record resolved (early)"), (8, "grid dependency"),
+                    (9, "first Q load issued"), (2, "first K/V TMA issued"), (10, "first Q landed (MMA)")):
+        v = ctaf[:, e]
+        if (v > 0).any():
+            print(f"  CTA start -> {name}: median {np.median(v[v > 0] - ctaf[v > 0, 0]) / 1e3:.2f} us")
     cta5 = tr.view(cap, 16).cpu().numpy()[3000:3000 + 148, :5].astype(np.int64)
     if cta5[:, 4].any():  # built with -DTAPER_TRACE_ITEMS: items / tiles per CTA
         end = (cta5[:, 1] - g0) / 1e3
