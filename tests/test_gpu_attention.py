@@ -413,3 +413,44 @@ def test_build_work_from_broadcast_mask_matches_admit():
     T.taper_decode_attention(db, adm3, kv, q, out3, None, case.scale, ws)
     torch.cuda.synchronize()
     _check_all(case, adm3, out3.cpu(), None, heads=[3, 40], what="build_work mask")
+
+
+@pytest.mark.parametrize("variant", ["flat", "peaked"])
+def test_row_mode_widths_groups_and_invariance(variant):
+    """Row mode (requests with >= 9 ready slots: 128 stacked rows on the MMA's M, P in TMEM,
+    DESIGN.md Sec. 6; reading R-mode): 9 to 33 ready branches (one or three 16-branch groups
+    per prefix chunk), ragged prefixes over several chunks, local segments crossing pages, and
+    partial admission (Cap 1 / 2 / 5: a row item with 8-40 live rows of 128).  Every admitted
+    row against the fp64 oracle, and the common slots bitwise equal across the admitted widths
+    (Sec. 3.1 / Lemma 1: the mode depends on n_r, not on w_r)."""
+    rng = np.random.default_rng(21)
+    lsh = [5000, 300, 4097, 65, 1800, 9100]
+    fan = [9, 13, 16, 17, 24, 33]
+    loc = rng.integers(1, 400, size=sum(fan)).tolist()
+    b = synth.make_batch(lsh, fan, loc, 1e3, 0.0, rng=rng)
+    case = Case(b, page=64, seed=9, variant=variant)
+    outs = {}
+    for policy, cap in (("eager", 2), ("cap", 1), ("cap", 2), ("cap", 5)):
+        adm, out, lse = case.run_gpu(policy=policy, cap=cap)
+        mask = adm.slot_admitted.cpu().numpy()[:b.n_slot].astype(bool)
+        _check_all(case, adm, out, lse, heads=range(0, 64, 3), what=f"row {variant} {policy}{cap}")
+        outs[(policy, cap)] = (mask, out)
+    m_e, o_e = outs[("eager", 2)]
+    for key in (("cap", 1), ("cap", 2), ("cap", 5)):
+        m, o = outs[key]
+        both = torch.from_numpy(m & m_e)
+        assert both.sum() > 0 and torch.equal(o[both], o_e[both]), key
+
+
+def test_row_mode_one_rank_of_8_heads():
+    """Row items on a rank holding one KV head (h = 1, 1024-token chunks at the batch size)
+    match the same heads of the oracle."""
+    rng = np.random.default_rng(23)
+    b = synth.make_batch([3000, 12000], [11, 16], rng.integers(1, 300, size=27).tolist(), 1e3, 0.0, rng=rng)
+    case = Case(b, seed=12)
+    for g in (0, 5):
+        adm, out, _ = case.run_gpu(policy="eager", heads=(g, g + 1), with_lse=False)
+        slots = np.flatnonzero(adm.slot_admitted.cpu().numpy()[:b.n_slot])
+        es, eh = np.repeat(slots, 8), np.tile(np.arange(8), len(slots))
+        ref, _ = case.run_oracle(es, eh + 8 * g)
+        assert_close(out[es, eh].float().numpy(), ref, f"row h=1 head {g}")
