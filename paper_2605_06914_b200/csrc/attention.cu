@@ -663,8 +663,9 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
 #else
 #define TAPER_ROW_INLINE __forceinline__
 #endif
-// (Out of line by default: a separate function keeps the swap-mode softmax code of the kernel
-// body contiguous; inlined, the extra ~600 instructions slowed swap-only layers by ~1.7 %.)
+// (TAPER_ROW_NOINLINE=1 moves it out of line: measured worse -- a 320 B stack frame and
+// spills in the kernel -- so it is inlined; the 1.7 % a row path once cost swap-only
+// layers came from the MMA warp's loop, fixed there.)
 template <bool M128>
 __device__ TAPER_ROW_INLINE void softmax_item_row(const SoftmaxCtx C, const Item x,
                                                   uint32_t item_idx, uint32_t &n) {
