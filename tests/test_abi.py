@@ -60,3 +60,20 @@ def test_host_validation_without_gpu():
     with pytest.raises(T.TaperError):
         T.max_chunk_slots([5], [0, 2], [1], h_local=8)
     assert T.max_chunk_slots([4097, 1, 0], [0, 3, 4, 6], [0, 65, 1, 0, 2, 3]) == 15 + 1 + 0 + 4
+
+
+def test_gather_and_ipc_host_validation_without_gpu():
+    """The fused-gather / IPC entry points (include/taper.h) reject bad arguments on the host
+    before touching the device."""
+    import ctypes
+    from paper_2605_06914_b200 import taper as T
+    lib = T._lib
+    # rank outside the world, world not a power of two up to 8, null flags
+    for world, rank in ((2, 2), (3, 0), (2, -1)):
+        g = T.Gather(world, 0, [0] * world, [0] * world)
+        g._c.rank = rank
+        assert lib.taper_gather_wait(ctypes.byref(g.c()), None) == T.TAPER_OK - 1  # TAPER_ERR_ARG
+    assert lib.taper_decode_attention_gather(None, None, None, None, None, None, 1.0, None, 0, None) == -1
+    assert lib.taper_ipc_handle(None, None, None) == -1
+    assert lib.taper_ipc_open(None, 0, None) == -1
+    assert lib.taper_ipc_close(None, 0) == -1
