@@ -204,6 +204,28 @@ __device__ __forceinline__ void tma_load_5d(void *smem_dst, const void *tmap, ui
       "r"(smem_u32(bar))
       : "memory");
 }
+// The same load with an L2 cache-policy hint (e.g. evict-first for KV tiles read once).
+__device__ __forceinline__ void tma_load_5d_hint(void *smem_dst, const void *tmap, uint64_t *bar,
+                                                 int c0, int c1, int c2, int c3, int c4,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+#ifndef TAPER_KV_EVICT_FRACTION
+#define TAPER_KV_EVICT_FRACTION 1.0
+#endif
+#define TAPER_STR2(x) #x
+#define TAPER_STR(x) TAPER_STR2(x)
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, " TAPER_STR(TAPER_KV_EVICT_FRACTION) ";"
+               : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void tma_prefetch_desc(const void *tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }
