@@ -7,23 +7,27 @@
 //
 //  A6+A7  attend_kernel (tcgen05 + TMA, one persistent CTA per SM, dynamic scheduling)
 //     Work items of one request r and local KV head g; the stacked query operand is
-//     Q^T = [8 GQA heads] x [w admitted branches] (N = 8 w <= 64 rows):
-//       * shared item : one chunk of P (+) H (taper_chunk_tokens(Lsh, h) <= 4096 tokens,
-//                       include/taper.h) for a group of <= 8 admitted
-//                       branches -- every page read ONCE from HBM and contracted against
-//                       all stacked rows (the cascade);
+//     [8 GQA heads] x [w admitted branches] (8 w <= 128 rows):
+//       * shared item : one chunk of P (+) H (taper_chunk_tokens(Lsh, h, R) <= 4096 tokens,
+//                       include/taper.h) for a group of <= 16 admitted branches -- every
+//                       page read ONCE from HBM and contracted against all stacked rows
+//                       (the cascade);
 //       * local item  : <= 16 64-token tiles of ONE admitted branch's h_i (+) y_i (w = 1),
 //                       or of one local segment of a reduce step's context (L104-107).
-//     Per 64-token tile, "swap-AB" (tokens on the MMA's M, stacked rows on N):
+//     Per 64-token tile, SWAP mode (requests with < 9 ready slots, local items; tokens on
+//     the MMA's M, stacked rows on N):
 //       S^T = K Q^T    tcgen05.mma SS, M = 64 tokens, N = 8 w, K = 128 (A = the K tile by
 //                      TMA, B = Q^T by TMA, both SMEM; fp32 S^T in TMEM)
 //       online softmax (two groups of 4 warps; lazy running max) -> P = hi + lo bf16,
 //                      stored transposed into SMEM with stmatrix.trans
 //       O^T += V^T P^T tcgen05.mma SS, M = 128 (d), N = 16 w (hi and lo rows), K = 64
 //                      (A = the V tile as an MN-major operand, B = P^T)
-//     so the tensor and softmax work of a tile scale with the live rows.  Output: a
-//     normalised partial (o, lse) per stacked row and item, published per (request, KV
-//     head) on a completion counter.
+//     so the tensor and softmax work of a tile scale with the live rows; ROW mode (requests
+//     with >= 9 ready slots; 128 stacked rows on M):
+//       S = Q K^T      SS, M = 128 rows, N = 64 tokens; softmax thread = row; P = hi + lo
+//                      to TMEM; O += P V as two TS MMAs (A = P from TMEM, B = the V tile).
+//     Output: a normalised partial (o, lse) per stacked row and item, published per
+//     (request, KV head) on a completion counter.
 //  A8     merge_kernel: per admitted slot and KV head, log-sum-exp merge of its partials
 //     (prefix chunks in order, then its local items) into bf16 out[s, 8g:8g+8, :];
 //     launched with PDL, each warp starts once its request's items are published.
@@ -48,7 +52,7 @@ constexpr int kItemTiles = (kChunk / kTileTokens > kLocalItemTiles) ? kChunk / k
 static_assert(kItemTiles <= 64, "scheduler lanes resolve at most two tiles each");
 // K and V tiles ride separate TMA rings: a K stage is released as soon as QK(t) completes,
 // a V stage only after PV(t); each stage is 64 tokens x 128 d bf16 = 16 KB.  Four + four
-// stages keep ~128 KB in flight per SM, as fast as five + five (same-box A/B, r2 ab_rings:
+// stages keep ~128 KB in flight per SM, as fast as 5 + 5 (same-box A/B, r2 ab_rings:
 // C2 191.3 vs 192.2 us, C3 846 vs 842 us) and they leave room for 16-branch Q operands.
 #ifndef TAPER_KSTAGES
 #define TAPER_KSTAGES 4
