@@ -42,3 +42,16 @@ def test_bench_line_contract():
     assert d["gpu_launches"] > 0 and d["config"]["workload"].startswith("c2")
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
+
+
+@pytest.mark.gpu
+def test_bench_c4_trace_replay_contract():
+    """--config c4: a (shortened) trace replay reports steps/s per load regime, and its
+    timed replay re-derived the first pass's admission bit for bit (asserted inside)."""
+    d = _run(["--config", "c4", "--c4-steps", "700", "--layers", "2", "--warmup", "3"])
+    assert d["config"]["workload"].startswith("c4") and d["steps"] == 700
+    regs = d["regimes"]
+    assert len(regs) == 3 and all(v["steps_per_s"] > 0 for v in regs.values())
+    rates = [v["opportunistic_admission_rate"] for v in regs.values()]
+    assert rates[0] > rates[1]  # low load admits more than the stress regime (P206-210)
+    assert d["gpu_launches"] > 0 and 0 < d["roofline"]["frac"] < 1.3
