@@ -39,8 +39,14 @@ def _rank_inputs(b, lay, k, v, qq, G, g, adm_mask, dev="cuda"):
     return db, adm, kv, q, ws
 
 
-def _case(seed=5):
-    b = synth.config_batch("c2", seed=seed, slack_min_ms=30.0)
+def _case(seed=5, kind="c2"):
+    if kind == "wide":  # requests with >= 9 ready slots: row-mode items
+        rng = np.random.default_rng(seed)
+        fan = [12, 1, 16, 9, 3, 1]
+        b = synth.make_batch([6000, 2500, 9000, 700, 4096, 1], fan,
+                             rng.integers(1, 300, size=sum(fan)).tolist(), 15.0, 20.0, rng=rng)  # partial: widths 9,1,1,9,3,1
+    else:
+        b = synth.config_batch("c2", seed=seed, slack_min_ms=30.0)
     lay = synth.make_layout(b, 64, np.random.default_rng(seed + 1), spare_pages=1)
     k, v = synth.make_kv(lay.num_pages, 8, 64, 128, seed=seed)
     qq = synth.make_q(b.n_slot, 64, 128, seed=seed)
@@ -63,11 +69,11 @@ def _per_rank_reference(b, lay, k, v, qq, G, mask):
     return torch.cat(parts, dim=1).cpu()
 
 
-@pytest.mark.parametrize("G", [2, 4, 8])
-def test_fused_gather_in_process(G):
+@pytest.mark.parametrize("G,kind", [(2, "c2"), (4, "c2"), (8, "c2"), (2, "wide"), (8, "wide")])
+def test_fused_gather_in_process(G, kind):
     from paper_2605_06914_b200 import parallel as par
     from paper_2605_06914_b200 import taper as T
-    b, lay, k, v, qq, mask = _case()
+    b, lay, k, v, qq, mask = _case(kind=kind)
     assert 0 < mask.sum() < b.n_slot
     ref = _per_rank_reference(b, lay, k, v, qq, G, mask)
     ranks = par.PeerGather.in_process(b.n_slot, G, n_buf=2, n_flag=2, device="cuda")
