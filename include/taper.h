@@ -92,10 +92,13 @@ extern "C" {
 #ifndef TAPER_CHUNK_TARGET
 #define TAPER_CHUNK_TARGET 512
 #endif
+#ifndef TAPER_CHUNK_MIN
+#define TAPER_CHUNK_MIN 1024
+#endif
 static inline TAPER_HD int32_t taper_chunk_tokens(int32_t lsh, int32_t h_local, int32_t n_req) {
   int64_t c = (int64_t)lsh * h_local * n_req / TAPER_CHUNK_TARGET;
   c = (c + 63) / 64 * 64;
-  if (c < 1024) c = 1024;
+  if (c < TAPER_CHUNK_MIN) c = TAPER_CHUNK_MIN;
   if (c > TAPER_CHUNK_TOKENS) c = TAPER_CHUNK_TOKENS;
   return (int32_t)c;
 }
