@@ -268,10 +268,11 @@ TAPER_API int taper_build_work(const taper_batch *batch, const taper_admission *
  * (NaN included): their scores are masked and their V rows zeroed before the PV product.
  * An admitted slot with an empty context writes zero rows (TAPER_STATUS_EMPTY_CONTEXT).
  * Ordering contract (programmatic dependent launch): the kernels may start while the
- * previous kernel on `stream` is still running.  They read the work list and the
- * admission outputs only after that kernel's writes are visible (a device-side epoch
- * that taper_admit / taper_build_work publishes is re-checked after the grid
- * dependency), and q / the K/V pools only after the grid dependency.  The page tables
+ * previous kernel on `stream` is still running.  A work item may be resolved from the
+ * work list before the grid dependency, but is used only after every work-list word it
+ * was resolved from has been read again after the dependency and found unchanged
+ * (otherwise it is resolved again); q / the K/V pools are read only after the grid
+ * dependency.  The page tables
  * (req_page_off ... seg_page_off) and the lengths in `batch` may be read early: they
  * must be written before the taper_admit / taper_build_work call that produced the work
  * list is enqueued (between that call and the attention calls only q and the K/V pool

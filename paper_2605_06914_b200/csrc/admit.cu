@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
       for (int i = tid; i < D; i += blockDim.x) p.sorted[i] = p.items[i];
     }
   }
-  __syncthreads();  // every table above is written before the epoch below publishes it
+  __syncthreads();  // every table above is written before the header below
   if (tid == 0) {
     int st = sh_status;
     int n_rc = tot_nc, n_rl = tot_nl;
@@ -685,11 +685,6 @@ __global__ void __launch_bounds__(kAdmitThreads, 1) admit_kernel(AdmitParams p) 
     p.hdr[9] = 0;  // attend CTAs exited
     *p.n_adm = n_adm;
     *p.status = st;  // the caller owns the word for this step (admit and build_work alike)
-    // Work-list epoch: attend_kernel resolves its first item before its grid dependency
-    // resolves (PDL) and re-checks this epoch afterwards; the release orders every write
-    // of this kernel (the barrier above) before the new epoch becomes visible.
-    __threadfence();
-    st_release(p.hdr + kHdrEpoch, ld_acquire(p.hdr + kHdrEpoch) + 1);
   }
 }
 

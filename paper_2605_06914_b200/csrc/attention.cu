@@ -60,8 +60,8 @@ static_assert(kItemTiles <= 64, "scheduler lanes resolve at most two tiles each"
 #ifndef TAPER_VSTAGES
 #define TAPER_VSTAGES 4
 #endif
-#ifndef TAPER_EARLY_CLAIM
-#define TAPER_EARLY_CLAIM 1
+#ifndef TAPER_PDL
+#define TAPER_PDL 1  // 0: attend_kernel launches without PDL (A/B experiments)
 #endif
 // Row mode (kItemRow, taper_internal.cuh): stacked rows on the MMA's M, S = Q K^T, thread =
 // row, P kept in TMEM for a TS MMA O += P V.  Swap mode: tokens on M ("swap-AB"), tensor and
@@ -69,7 +69,6 @@ static_assert(kItemTiles <= 64, "scheduler lanes resolve at most two tiles each"
 // every local item (w = 1).  See DESIGN.md "row mode".
 constexpr int kSwapMaxW = kRowMin - 1;       // widest swap-mode item
 constexpr int kSwapMaxWB = (kSwapMaxW + 1) / 2;  // 8-row blocks per softmax group (swap mode)
-constexpr bool kEarlyClaim = TAPER_EARLY_CLAIM;
 constexpr int kKStages = TAPER_KSTAGES;
 constexpr int kVStages = TAPER_VSTAGES;
 constexpr int kStageBytes = 2 * 8192;
@@ -214,6 +213,7 @@ __device__ __forceinline__ void decode_item(const ItemRec *rec, Item &x) {
 struct TileInfo {
   const int32_t *pages;
   int tok0, valid;
+  int4 lt;  // local item: the work-list entry the tile was resolved from
 };
 
 __device__ __forceinline__ TileInfo tile_info(const AttnParams &p, const Item &x, int t) {
@@ -221,9 +221,11 @@ __device__ __forceinline__ TileInfo tile_info(const AttnParams &p, const Item &x
   if (!x.local) {
     ti.pages = p.req_pages + __ldcg(p.req_page_off + x.r);
     ti.tok0 = x.tb + t * kTile;
+    ti.lt = make_int4(0, 0, 0, 0);
     ti.valid = min(kTile, x.te - ti.tok0);
   } else {
     const int4 lt = __ldcg(p.ltiles + x.tb + t);  // {slot, tok0, valid, segment or -1}
+    ti.lt = lt;
     ti.pages = p.slot_pages + __ldcg(p.slot_page_off + (lt.w >= 0 ? lt.w : lt.x));
     ti.tok0 = lt.y;
     ti.valid = lt.z;
@@ -886,7 +888,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   // the merge kernel launch (it reads the work list, which is complete and visible once
   // this grid's dependency has resolved; its warps then wait for per-request completion
   // counters).  The scheduler warp resolves its first item before waiting (see below).
-  if (!(kEarlyClaim && warp == 11)) {
+  if (warp != 11) {
     pdl_wait();
     pdl_launch_dependents();
   }
@@ -899,18 +901,27 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // Q^T (one 2 KB TMA box per branch: its 8 GQA rows, SW128) into Q buffer k & 1.  The
     // dependent global loads of an item thus overlap the previous item.
     const int box_tok = p.page_size < kTile ? p.page_size : kTile;
-    // Work-list epoch (hdr[10]), read with acquire BEFORE any table: if it is the epoch of
-    // the admission that wrote the tables, those tables are visible; if that admission is
-    // the kernel still draining in front of this one, the epoch moves before the re-check
-    // below and the first item is resolved again (include/taper.h ordering contract).
-    int epoch = kEarlyClaim ? ld_acquire(p.hdr + kHdrEpoch) : 0;
-    if (lane == 0) trace_cta_dep(p, 11, epoch);  // epoch (acquire) loaded
-    // items per KV head, or none if the work list was written for another workspace / h
-    auto count_items = [&]() {
-      const bool ok = __ldcg(p.hdr + 4) == h && __ldcg(p.hdr + 3) == p.cap_cs;
-      return ok ? (__ldcg(p.hdr) + __ldcg(p.hdr + 5)) * h : 0;
+    // The first item is resolved speculatively, before the grid dependency, from plain
+    // loads of the work list issued all at once (no acquire chain); after the dependency
+    // resolves, every work-list word the record was built from is read again and compared
+    // (include/taper.h ordering contract): equal values give the same record, otherwise it
+    // is resolved again from the values now visible.
+    // Control snapshot: one work-list word per lane from a fixed address -- lanes 0-7 the
+    // descriptor of claim index blockIdx.x, 8-11 header words -- so the first item costs one
+    // load latency before its pages, and validating it after the grid dependency another.
+    const int32_t *snap_addr =
+        lane < 8 ? reinterpret_cast<const int32_t *>(
+                       p.sorted + min(int(blockIdx.x) / h, p.cap_cs > 0 ? p.cap_cs - 1 : 0)) + lane
+                 : p.hdr + (lane == 8 ? 0 : lane == 9 ? 5 : lane == 10 ? 3 : lane == 11 ? 4 : 0);
+    int32_t snap = __ldcg(snap_addr);
+    // claims per launch (items x KV heads), or none if the work list was written for another
+    // workspace / h_local (warp-uniform)
+    int n_items = 0;
+    auto derive = [&]() {
+      const bool ok = __shfl_sync(0xffffffffu, snap, 11) == h && __shfl_sync(0xffffffffu, snap, 10) == p.cap_cs;
+      n_items = ok ? (__shfl_sync(0xffffffffu, snap, 8) + __shfl_sync(0xffffffffu, snap, 9)) * h : 0;
     };
-    int n_items = count_items();
+    derive();
     if (lane == 0) trace_cta_dep(p, 12, n_items);  // header loaded
     int *work_counter = p.hdr + 8;
     // the descriptor of claim index `it` (longest first, then KV head), loaded before the
@@ -924,6 +935,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // claim index `it` (-1: none) -> the SMEM record (descriptor, per-tile geometry and
     // pages); slot_j = the admitted slot of the item's branch `lane` (its Q rows), loaded
     // alongside the pages
+    int4 lt_seen = make_int4(0, 0, 0, 0);  // local item: the entry of tile `lane`
     auto resolve = [&](ItemRec *rec, int it, int32_t d, int &w, int &adm_off, int &g, int &slot_j) {
       w = 0; adm_off = 0; g = 0; slot_j = 0;
       if (it >= 0) {
@@ -941,6 +953,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         if (lane < w) slot_j = __ldcg(p.adm_by_req + adm_off + lane);
         for (int t = lane; t < nt; t += 32) {
           const TileInfo ti = tile_info(p, x, t);
+          if (t == lane) lt_seen = ti.lt;
           rec->tok0[t] = ti.tok0;
           rec->valid[t] = ti.valid;
 #pragma unroll
@@ -951,35 +964,48 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       if (lane == 0) { rec->it = it; rec->g = g; }
     };
+    // claim index of the k-th item of this CTA: blockIdx.x first, then from the counter
+    auto claim = [&](uint32_t k) -> int {
+      int c = int(blockIdx.x);
+      if (k > 0 && lane == 0) c = int(gridDim.x) + atomicAdd(work_counter, 1);
+      return __shfl_sync(0xffffffffu, c, 0);
+    };
+    auto first_desc = [&]() -> int32_t { return lane < 8 ? snap : 0; };
     for (uint32_t k = 0;; ++k) {
       if (k >= 1) mbar_wait(sched_go, (k - 1) & 1);  // K producer started item k-1
-      int it = 0;
-      // first item: claim index blockIdx.x (static), later ones from the counter
-      if (lane == 0)
-        it = (kEarlyClaim && k == 0) ? int(blockIdx.x)
-                                     : (kEarlyClaim ? int(gridDim.x) : 0) + atomicAdd(work_counter, 1);
-      it = __shfl_sync(0xffffffffu, it, 0);
-      int32_t d = load_desc(it);
+      int it = claim(k);
+      int32_t d = k == 0 ? first_desc() : load_desc(it);
       if (k == 0 && lane == 0) trace_cta_dep(p, 13, d);  // descriptor loaded
       const uint32_t slot = k % kItemRing;
       ItemRec *rec = recs + slot;
       mbar_wait(it_empty + slot, ((k / kItemRing) & 1) ^ 1);
       int w, adm_off, g, slot_j;
-      for (bool early = kEarlyClaim && k == 0;;) {
+      for (bool early = k == 0;;) {
         resolve(rec, it < n_items ? it : -1, d, w, adm_off, g, slot_j);
         if (k == 0 && lane == 0) trace_cta(p, early ? 6 : 7);  // first record resolved
         if (!early) break;
         // The first record was resolved while the previous kernel drained.  Now wait for
         // it (q, the K/V pools and a just-written work list become visible), let the merge
-        // kernel launch, and re-resolve if an admission published a new work list meanwhile.
+        // kernel launch, and validate: the header, the descriptor, the branches' slots and
+        // (local item) the tile entries are loaded again -- independent loads, one latency
+        // -- and compared with the values the record was resolved from.
         early = false;
         pdl_wait();
         pdl_launch_dependents();
         if (lane == 0) trace_cta(p, 8);  // grid dependency resolved
-        if (ld_acquire(p.hdr + kHdrEpoch) == epoch) break;
-        n_items = count_items();
-        d = load_desc(it);
-        __syncwarp();
+        const int32_t snap2 = __ldcg(snap_addr);
+        const bool was_item = it >= 0 && it < n_items;
+        const int nt_e = __shfl_sync(0xffffffffu, d, 6), tb_e = __shfl_sync(0xffffffffu, d, 4);
+        const bool local_e = __shfl_sync(0xffffffffu, d, 7) & kItemLocal;
+        const int sj2 = (was_item && lane < w) ? __ldcg(p.adm_by_req + adm_off + lane) : slot_j;
+        const int4 lt2 = (was_item && local_e && lane < nt_e) ? __ldcg(p.ltiles + tb_e + lane) : lt_seen;
+        const bool same = (snap2 == snap) & (sj2 == slot_j) & (lt2.x == lt_seen.x) &
+                          (lt2.y == lt_seen.y) & (lt2.z == lt_seen.z) & (lt2.w == lt_seen.w);
+        if (__all_sync(0xffffffffu, same)) break;
+        snap = snap2;
+        derive();
+        it = claim(0);
+        d = first_desc();
       }
       if (it >= n_items) it = -1;
       __syncwarp();
@@ -1710,7 +1736,7 @@ static int decode_attention(const taper_batch *batch, const taper_admission *adm
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
   cfg.attrs = pdl;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = TAPER_PDL ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, attend_kernel, tmK, tmV, tmK16, tmV16, tmQ, ap);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail_cuda(e, "attend_kernel launch");

@@ -27,8 +27,6 @@ constexpr int kMaxItemBranches = 16;  // admitted branches stacked in one shared
 // hdr[5] = n_rl    : number of (request, local item) pairs (local items per KV head)
 // hdr[8] = work counter of attend_kernel's dynamic scheduler (reset by admit and by the
 //          last attend CTA to exit, counted in hdr[9])
-// hdr[10] = work-list epoch, incremented (release) by every admit / build_work as its last
-//          write; attend_kernel's early first claim is validated against it
 struct WsLayout {
   size_t hdr, slot_req, slot_rank, slot_lbase, req_chunk_off, req_loc_off, req_part_off,
       req_adm_off, adm_by_req, merge_desc, done, part_lse, part_o, fixed;
@@ -178,7 +176,6 @@ __device__ __forceinline__ int ld_acquire(const int32_t *p) {
 __device__ __forceinline__ void st_release(int32_t *p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-constexpr int kHdrEpoch = 10;
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

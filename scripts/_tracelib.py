@@ -11,5 +11,6 @@ if "TAPER_LIB" not in os.environ:
     from paper_2605_06914_b200 import build as _b
     _out = os.path.join(ROOT, "build", "libtaper_trace.so")
     os.makedirs(os.path.dirname(_out), exist_ok=True)
-    _b.build(force=True, defines=["TAPER_TRACE=1"], out=_out)
+    _b.build(force=True, defines=["TAPER_TRACE=1", *filter(None, os.environ.get("TAPER_EXTRA_DEFINES", "").split(","))],
+             out=_out)
     os.environ["TAPER_LIB"] = _out
