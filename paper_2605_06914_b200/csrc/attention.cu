@@ -60,6 +60,9 @@ static_assert(kItemTiles <= 64, "scheduler lanes resolve at most two tiles each"
 #ifndef TAPER_VSTAGES
 #define TAPER_VSTAGES 4
 #endif
+#ifndef TAPER_DBG_FORCE_RERESOLVE
+#define TAPER_DBG_FORCE_RERESOLVE 0  // test builds: always take the re-resolve path
+#endif
 #ifndef TAPER_PDL
 #define TAPER_PDL 1  // 0: attend_kernel launches without PDL (A/B experiments)
 #endif
@@ -367,6 +370,26 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t *>(&h2);
 }
+// P = hi + lo, both bf16 pairs.  kTrunc: hi is the upper half of
+// each fp32 word (one byte permute instead of a conversion), lo = P - hi rounded to bf16
+// (|error| <= 2^-16 P instead of 2^-17).  Swap mode truncates (same-box: C2 188.0 -> 186.1
+// us per layer, -0.7 % at the power cap); row mode rounds (truncating there measured 3 %
+// slower on C3).
+#ifndef TAPER_PHI_TRUNC_SWAP
+#define TAPER_PHI_TRUNC_SWAP 1
+#endif
+template <bool kTrunc>
+__device__ __forceinline__ void split_hi_lo(float a, float b, uint32_t &hi, uint32_t &lo) {
+  if constexpr (kTrunc) {
+    const uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+    hi = __byte_perm(ua, ub, 0x7632);
+    lo = pack_bf16(a - __uint_as_float(ua & 0xffff0000u), b - __uint_as_float(ub & 0xffff0000u));
+  } else {
+    hi = pack_bf16(a, b);
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&hi));
+    lo = pack_bf16(a - f.x, b - f.y);
+  }
+}
 
 // Butterfly plan for NC columns over lane bits 4, 3, 2: an even count is halved by a
 // transposing exchange (each lane keeps one half), an odd one is reduced in place.
@@ -553,13 +576,8 @@ __device__ __forceinline__ void softmax_item(const SoftmaxCtx &C, const ItemRec 
           pB[e] = ex2(fmaf(x2[4 * b + 2 + e], C.c, neg_m));
           l_run[i] += pA[e] + pB[e];
         }
-        const uint32_t hA = pack_bf16(pA[0], pA[1]), hB = pack_bf16(pB[0], pB[1]);
-        const float2 fA = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&hA));
-        const float2 fB = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&hB));
-        pk[4 * b] = hA;
-        pk[4 * b + 1] = hB;
-        pk[4 * b + 2] = pack_bf16(pA[0] - fA.x, pA[1] - fA.y);
-        pk[4 * b + 3] = pack_bf16(pB[0] - fB.x, pB[1] - fB.y);
+        split_hi_lo<TAPER_PHI_TRUNC_SWAP>(pA[0], pA[1], pk[4 * b], pk[4 * b + 2]);
+        split_hi_lo<TAPER_PHI_TRUNC_SWAP>(pB[0], pB[1], pk[4 * b + 1], pk[4 * b + 3]);
       }
       if (C.warp == 2 && lane == 0) trace_ev(*C.p, 10, n);
       // the P^T (half) buffer this tile writes was last read by PV(n-2) when this and the
@@ -721,12 +739,12 @@ __device__ TAPER_ROW_INLINE void softmax_item_row(const SoftmaxCtx C, const Item
 #pragma unroll
       for (int i = 0; i < NT / 2; ++i) {
         const float pA = ex2(fmaf(xv[2 * i], C.c, neg_m)), pB = ex2(fmaf(xv[2 * i + 1], C.c, neg_m));
-        pk[i] = pack_bf16(pA, pB);
-        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&pk[i]));
         if constexpr (kRowPlo) {
-          pl[i] = pack_bf16(pA - f.x, pB - f.y);
+          split_hi_lo<false>(pA, pB, pk[i], pl[i]);
           ls += pA + pB;
         } else {
+          pk[i] = pack_bf16(pA, pB);
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&pk[i]));
           ls += f.x + f.y;  // the row sum of what the MMA multiplies
         }
       }
@@ -999,7 +1017,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const bool local_e = __shfl_sync(0xffffffffu, d, 7) & kItemLocal;
         const int sj2 = (was_item && lane < w) ? __ldcg(p.adm_by_req + adm_off + lane) : slot_j;
         const int4 lt2 = (was_item && local_e && lane < nt_e) ? __ldcg(p.ltiles + tb_e + lane) : lt_seen;
-        const bool same = (snap2 == snap) & (sj2 == slot_j) & (lt2.x == lt_seen.x) &
+        const bool same = !TAPER_DBG_FORCE_RERESOLVE & (snap2 == snap) & (sj2 == slot_j) & (lt2.x == lt_seen.x) &
                           (lt2.y == lt_seen.y) & (lt2.z == lt_seen.z) & (lt2.w == lt_seen.w);
         if (__all_sync(0xffffffffu, same)) break;
         snap = snap2;
