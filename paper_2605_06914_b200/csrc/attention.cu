@@ -63,6 +63,12 @@ static_assert(kItemTiles <= 64, "scheduler lanes resolve at most two tiles each"
 #ifndef TAPER_DBG_FORCE_RERESOLVE
 #define TAPER_DBG_FORCE_RERESOLVE 0  // test builds: always take the re-resolve path
 #endif
+#ifndef TAPER_MERGE_PDL
+#define TAPER_MERGE_PDL 1  // 0: merge_kernel launches without PDL (A/B experiments)
+#endif
+#ifndef TAPER_MERGE_GRID
+#define TAPER_MERGE_GRID 0  // > 0: at most this many merge CTAs (A/B experiments)
+#endif
 #ifndef TAPER_PDL
 #define TAPER_PDL 1  // 0: attend_kernel launches without PDL (A/B experiments)
 #endif
@@ -1782,8 +1788,10 @@ static int decode_attention(const taper_batch *batch, const taper_admission *adm
     mp.gflags[j] = gather && j < gather->world ? gather->flags[j] : nullptr;
   }
   mp.gcount = ap.hdr + 11;
-  const int grid = S > 0 ? S : 1;  // CTAs beyond the admitted count exit at once
+  int grid = S > 0 ? S : 1;  // CTAs beyond the admitted count exit at once
+  if (TAPER_MERGE_GRID > 0 && grid > TAPER_MERGE_GRID) grid = TAPER_MERGE_GRID;  // (A/B knob)
   cfg.gridDim = dim3(grid);
+  cfg.numAttrs = TAPER_MERGE_PDL ? 1 : 0;
   cfg.blockDim = dim3(kMergeThreads);
   cfg.dynamicSmemBytes = 0;
   e = cudaLaunchKernelEx(&cfg, merge_kernel, mp);
