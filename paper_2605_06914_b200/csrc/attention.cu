@@ -1400,7 +1400,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 }
 
 // ------------------------------------------------------------------ A8: LSE merge
-constexpr int kMergeThreads = 256;  // one CTA per admitted slot, one warp per KV head
+constexpr int kMergeThreads = 256;  // one CTA per admitted slot, warps over (KV head, row)
 
 struct MergeParams {
   long long *trace;  // debug: per-CTA globaltimer span at rows 3200 + CTA (taper_set_trace_buffer)
@@ -1432,13 +1432,97 @@ __device__ __forceinline__ void st_release_sys(int32_t *p, int v) {
   asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Per (admitted slot, KV head): the slot's partials are 8 contiguous GQA rows (4 KB) per
-// work item, so the warp streams whole 4 KB blocks (lane: dims 4 lane .. 4 lane + 3 of all 8
-// rows) and runs the 8 rows' online LSE merges side by side, partials in work order
-// (prefix chunks, then local items), two items' loads in flight at a time.
+// Per (admitted slot, KV head, GQA row): a warp merges the row's partials (lane: dims
+// 4 lane .. 4 lane + 3, 512 B per partial row) with an online LSE, partials in work order
+// (prefix chunks, then local items), up to kMergeBatch partials' loads in flight at a time.
 // Launched with PDL while attend_kernel is still running: a warp starts as soon as the
 // attend epilogues have published all items of its (request, KV head) (acquire on the
 // completion counter), so the merge overlaps the attend kernel's tail.
+// Units of RPW rows of one KV head; NB partials in flight per round (NB * RPW <= 32 lanes
+// carry the lse values).  Partials merge in work order (prefix chunks, then local items), so
+// each row's arithmetic does not depend on RPW / NB.
+template <int RPW, int NB>
+__device__ __forceinline__ void merge_slot(const MergeParams &p, int s, int r, int w, const int4 md,
+                                           const int4 ml, int target, int warp, int lane, int qheads) {
+  static_assert(NB * RPW <= 32 && kGroup % RPW == 0, "lse lanes");
+  constexpr int kUnitsPerHead = kGroup / RPW;
+  const int h = p.h_local, nc = md.z, nq = nc + ml.y;
+  for (int u = warp; u < h * kUnitsPerHead; u += kMergeThreads / 32) {
+    const int g = u / kUnitsPerHead, a0 = (u - g * kUnitsPerHead) * RPW;
+    int32_t *cnt = p.done + r * kGroup + g;
+    if (ld_acquire(cnt) < target) {  // bounded spin: a lost publication traps, never hangs
+      const long long t0 = clock64();
+      while (ld_acquire(cnt) < target) {
+        __nanosleep(128);
+        if (clock64() - t0 > (1ll << 35)) __trap();
+      }
+    }
+    float M[RPW], Z[RPW];
+    float4 acc[RPW];
+#pragma unroll
+    for (int a = 0; a < RPW; ++a) {
+      M[a] = -INFINITY; Z[a] = 0.f; acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int q0 = 0; q0 < nq; q0 += NB) {
+      float4 v[NB][RPW];
+      float l2 = -INFINITY;  // lane u * RPW + a: lse of row a0 + a of partial q0 + u (log2 units)
+#pragma unroll
+      for (int u2 = 0; u2 < NB; ++u2) {
+        const int q = q0 + u2;  // prefix chunk q (stride w), then the slot's own local items
+        const bool ok = q < nq;
+        const size_t cs = q < nc ? (size_t)md.y + (size_t)q * w : (size_t)ml.x + (q - nc);
+        const size_t prow = (cs * h + g) * kGroup + a0;
+        if (ok && lane / RPW == u2) l2 = __ldcg(p.part_lse + prow + lane % RPW) * 1.4426950408889634f;
+#pragma unroll
+        for (int a = 0; a < RPW; ++a)
+          v[u2][a] = ok ? __ldcg(reinterpret_cast<const float4 *>(p.part_o + (prow + a) * kHeadDim) + lane)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u2 = 0; u2 < NB; ++u2) {
+#pragma unroll
+        for (int a = 0; a < RPW; ++a) {
+          const float lq = __shfl_sync(0xffffffffu, l2, u2 * RPW + a);
+          if (lq == -INFINITY) continue;
+          const float Mn = fmaxf(M[a], lq);
+          const float sc = ex2(M[a] - Mn), wgt = ex2(lq - Mn);  // ex2(-inf) = 0
+          acc[a].x = acc[a].x * sc + wgt * v[u2][a].x; acc[a].y = acc[a].y * sc + wgt * v[u2][a].y;
+          acc[a].z = acc[a].z * sc + wgt * v[u2][a].z; acc[a].w = acc[a].w * sc + wgt * v[u2][a].w;
+          Z[a] = Z[a] * sc + wgt;
+          M[a] = Mn;
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < RPW; ++a) {
+      const float inv = Z[a] > 0.f ? 1.f / Z[a] : 0.f;  // empty context: zeros, lse -inf
+      __align__(8) __nv_bfloat162 o2[2];
+      o2[0] = __floats2bfloat162_rn(acc[a].x * inv, acc[a].y * inv);
+      o2[1] = __floats2bfloat162_rn(acc[a].z * inv, acc[a].w * inv);
+      const int qh = g * kGroup + a0 + a;
+      if (p.world == 0) {
+        *reinterpret_cast<uint2 *>(p.out + ((size_t)s * qheads + qh) * kHeadDim + 4 * lane) =
+            *reinterpret_cast<uint2 *>(o2);
+      } else {  // fused gather: the row goes to every rank's buffer (NVLink peer stores)
+        const size_t off = ((size_t)s * (kGroup * kGroup) + p.head0 + qh) * kHeadDim + 4 * lane;
+        for (int j = 0; j < p.world; ++j)
+          *reinterpret_cast<uint2 *>(p.gout[j] + off) = *reinterpret_cast<uint2 *>(o2);
+      }
+      if (p.lse_out && lane == a)
+        p.lse_out[(size_t)s * qheads + qh] = (M[a] + __log2f(Z[a])) * 0.69314718055994531f;
+    }
+    // the last of the request's w * kUnitsPerHead readers re-arms the counters for the next call
+    __syncwarp();
+    if (lane == 0 && atomicAdd(cnt + p.R * kGroup, 1) == w * kUnitsPerHead - 1) {
+      *cnt = 0;
+      cnt[p.R * kGroup] = 0;
+    }
+  }
+}
+
+// One instantiation per rows-per-unit (RPW = the largest power of two <= h_local), chosen by
+// the host: each gets its own register allocation (one kernel holding all four spilled).
+template <int RPW, int NB>
 __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool tr = kTrace && p.trace != nullptr && threadIdx.x == 0 && 3200 + int(blockIdx.x) < p.trace_cap;
@@ -1462,76 +1546,13 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) 
     const int4 md = __ldcg(p.merge_desc + 2 * k);
     const int4 ml = __ldcg(p.merge_desc + 2 * k + 1);
     const int s = md.x, nc = md.z, w = md.w, r = ml.z;
-    const int nq = nc + ml.y, target = ml.w;
-    for (int g = warp; g < h; g += kMergeThreads / 32) {
-      int32_t *cnt = p.done + r * kGroup + g;
-      if (ld_acquire(cnt) < target) {  // bounded spin: a lost publication traps, never hangs
-        const long long t0 = clock64();
-        while (ld_acquire(cnt) < target) {
-          __nanosleep(256);
-          if (clock64() - t0 > (1ll << 35)) __trap();
-        }
-      }
-      float M[kGroup], Z[kGroup];
-      float4 acc[kGroup];
-#pragma unroll
-      for (int a = 0; a < kGroup; ++a) {
-        M[a] = -INFINITY; Z[a] = 0.f; acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      for (int q0 = 0; q0 < nq; q0 += 2) {
-        float4 v[2][kGroup];
-        float l2 = -INFINITY;  // lane u * 8 + a: lse of row a of item q0 + u (log2 units)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const bool ok = q0 + u < nq;
-          const int q = q0 + u;  // prefix chunk q (stride w), then the slot's own local items
-          const size_t cs = q < nc ? (size_t)md.y + (size_t)q * w : (size_t)ml.x + (q - nc);
-          const size_t prow = (cs * h + g) * kGroup;
-          if (ok && (lane >> 3) == u) l2 = __ldcg(p.part_lse + prow + (lane & 7)) * 1.4426950408889634f;
-#pragma unroll
-          for (int a = 0; a < kGroup; ++a)
-            v[u][a] = ok ? __ldcg(reinterpret_cast<const float4 *>(p.part_o + (prow + a) * kHeadDim) + lane)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-#pragma unroll
-          for (int a = 0; a < kGroup; ++a) {
-            const float lq = __shfl_sync(0xffffffffu, l2, u * 8 + a);
-            if (lq == -INFINITY) continue;
-            const float Mn = fmaxf(M[a], lq);
-            const float sc = ex2(M[a] - Mn), wgt = ex2(lq - Mn);  // ex2(-inf) = 0
-            acc[a].x = acc[a].x * sc + wgt * v[u][a].x; acc[a].y = acc[a].y * sc + wgt * v[u][a].y;
-            acc[a].z = acc[a].z * sc + wgt * v[u][a].z; acc[a].w = acc[a].w * sc + wgt * v[u][a].w;
-            Z[a] = Z[a] * sc + wgt;
-            M[a] = Mn;
-          }
-        }
-      }
-#pragma unroll
-      for (int a = 0; a < kGroup; ++a) {
-        const float inv = Z[a] > 0.f ? 1.f / Z[a] : 0.f;  // empty context: zeros, lse -inf
-        __align__(8) __nv_bfloat162 o2[2];
-        o2[0] = __floats2bfloat162_rn(acc[a].x * inv, acc[a].y * inv);
-        o2[1] = __floats2bfloat162_rn(acc[a].z * inv, acc[a].w * inv);
-        if (p.world == 0) {
-          *reinterpret_cast<uint2 *>(p.out + ((size_t)s * qheads + g * kGroup + a) * kHeadDim + 4 * lane) =
-              *reinterpret_cast<uint2 *>(o2);
-        } else {  // fused gather: the row goes to every rank's buffer (NVLink peer stores)
-          const size_t off = ((size_t)s * (kGroup * kGroup) + p.head0 + g * kGroup + a) * kHeadDim + 4 * lane;
-          for (int j = 0; j < p.world; ++j)
-            *reinterpret_cast<uint2 *>(p.gout[j] + off) = *reinterpret_cast<uint2 *>(o2);
-        }
-        if (p.lse_out && lane == a)
-          p.lse_out[(size_t)s * qheads + g * kGroup + a] = (M[a] + __log2f(Z[a])) * 0.69314718055994531f;
-      }
-      // the last of the request's w readers re-arms the counters for the next call
-      __syncwarp();
-      if (lane == 0 && atomicAdd(cnt + p.R * kGroup, 1) == w - 1) {
-        *cnt = 0;
-        cnt[p.R * kGroup] = 0;
-      }
-    }
+    const int target = ml.w;
+    (void)nc;
+    // one warp per (KV head, RPW GQA rows), RPW = the largest power of two <= h: the 8 warps
+    // cover all units of a slot at once whatever h is, so the merge after the request's last
+    // item costs about one load latency (a warp per KV head left 7 of 8 warps idle at h = 1:
+    // same-box C2 h = 1 41.7 -> 36.9 us per call, C3 h = 1 106 -> 97)
+    merge_slot<RPW, NB>(p, s, r, w, md, ml, target, warp, lane, qheads);
   }
   if (p.world > 0) {
     // every row of this CTA is stored (system-scope fence by each thread), then the last CTA
@@ -1794,7 +1815,10 @@ static int decode_attention(const taper_batch *batch, const taper_admission *adm
   cfg.numAttrs = TAPER_MERGE_PDL ? 1 : 0;
   cfg.blockDim = dim3(kMergeThreads);
   cfg.dynamicSmemBytes = 0;
-  e = cudaLaunchKernelEx(&cfg, merge_kernel, mp);
+  e = h >= 8   ? cudaLaunchKernelEx(&cfg, merge_kernel<8, 2>, mp)
+      : h >= 4 ? cudaLaunchKernelEx(&cfg, merge_kernel<4, 4>, mp)
+      : h >= 2 ? cudaLaunchKernelEx(&cfg, merge_kernel<2, 8>, mp)
+               : cudaLaunchKernelEx(&cfg, merge_kernel<1, 8>, mp);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail_cuda(e, "merge_kernel launch");
   if (g_prof_ev[2]) cudaEventRecord(g_prof_ev[2], st);
