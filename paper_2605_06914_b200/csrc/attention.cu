@@ -1443,11 +1443,12 @@ __device__ __forceinline__ void st_release_sys(int32_t *p, int v) {
 // each row's arithmetic does not depend on RPW / NB.
 template <int RPW, int NB>
 __device__ __forceinline__ void merge_slot(const MergeParams &p, int s, int r, int w, const int4 md,
-                                           const int4 ml, int target, int warp, int lane, int qheads) {
+                                           const int4 ml, int target, int warp, int wps, int lane,
+                                           int qheads) {
   static_assert(NB * RPW <= 32 && kGroup % RPW == 0, "lse lanes");
   constexpr int kUnitsPerHead = kGroup / RPW;
   const int h = p.h_local, nc = md.z, nq = nc + ml.y;
-  for (int u = warp; u < h * kUnitsPerHead; u += kMergeThreads / 32) {
+  for (int u = warp; u < h * kUnitsPerHead; u += wps) {
     const int g = u / kUnitsPerHead, a0 = (u - g * kUnitsPerHead) * RPW;
     int32_t *cnt = p.done + r * kGroup + g;
     if (ld_acquire(cnt) < target) {  // bounded spin: a lost publication traps, never hangs
@@ -1522,6 +1523,10 @@ __device__ __forceinline__ void merge_slot(const MergeParams &p, int s, int r, i
 
 // One instantiation per rows-per-unit (RPW = the largest power of two <= h_local), chosen by
 // the host: each gets its own register allocation (one kernel holding all four spilled).
+#ifndef TAPER_MERGE_MIN_RPW
+#define TAPER_MERGE_MIN_RPW 1  // 2: two slots per merge CTA at h = 1 (A/B: C2, C3 slower, C5 faster)
+#endif
+constexpr int kMergeMinRpw = TAPER_MERGE_MIN_RPW;
 template <int RPW, int NB>
 __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1540,7 +1545,9 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) 
   if (!match && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(p.status, TAPER_STATUS_WORK_MISMATCH);
   const int n_adm = match ? __ldcg(p.hdr + 2) : 0;
   const int qheads = kGroup * h;
-  for (int k = blockIdx.x; k < n_adm; k += gridDim.x) {
+  // spc slots per CTA (RPW > h: a slot has fewer units than the CTA has warps), wps warps each
+  const int spc = RPW > h ? RPW / h : 1, wps = (kMergeThreads / 32) / spc;
+  for (int k = blockIdx.x * spc + warp / wps; k < n_adm; k += gridDim.x * spc) {
     // {slot, first shared partial, prefix chunks, width}, {first local partial, local items,
     // request, items of the request per KV head}
     const int4 md = __ldcg(p.merge_desc + 2 * k);
@@ -1552,7 +1559,7 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) 
     // cover all units of a slot at once whatever h is, so the merge after the request's last
     // item costs about one load latency (a warp per KV head left 7 of 8 warps idle at h = 1:
     // same-box C2 h = 1 41.7 -> 36.9 us per call, C3 h = 1 106 -> 97)
-    merge_slot<RPW, NB>(p, s, r, w, md, ml, target, warp, lane, qheads);
+    merge_slot<RPW, NB>(p, s, r, w, md, ml, target, warp % wps, wps, lane, qheads);
   }
   if (p.world > 0) {
     // every row of this CTA is stored (system-scope fence by each thread), then the last CTA
@@ -1815,10 +1822,15 @@ static int decode_attention(const taper_batch *batch, const taper_admission *adm
   cfg.numAttrs = TAPER_MERGE_PDL ? 1 : 0;
   cfg.blockDim = dim3(kMergeThreads);
   cfg.dynamicSmemBytes = 0;
-  e = h >= 8   ? cudaLaunchKernelEx(&cfg, merge_kernel<8, 2>, mp)
-      : h >= 4 ? cudaLaunchKernelEx(&cfg, merge_kernel<4, 4>, mp)
-      : h >= 2 ? cudaLaunchKernelEx(&cfg, merge_kernel<2, 8>, mp)
-               : cudaLaunchKernelEx(&cfg, merge_kernel<1, 8>, mp);
+  // rows per merge unit: the largest power of two <= h, at least kMergeMinRpw (2 at h = 1:
+  // one CTA takes two slots -- half the merge CTAs holding SMs the next call's attend CTAs
+  // need; same-box C5 h = 1 216.3 -> 213.3 us but C2 36.9 -> 38.3, C3 97.4 -> 101.0: off)
+  const int rpw = h >= 8 ? 8 : h >= 4 ? 4 : (h >= 2 || kMergeMinRpw >= 2) ? 2 : 1;
+  if (rpw > h) cfg.gridDim = dim3((grid + rpw / h - 1) / (rpw / h));
+  e = rpw == 8   ? cudaLaunchKernelEx(&cfg, merge_kernel<8, 2>, mp)
+      : rpw == 4 ? cudaLaunchKernelEx(&cfg, merge_kernel<4, 4>, mp)
+      : rpw == 2 ? cudaLaunchKernelEx(&cfg, merge_kernel<2, 8>, mp)
+                 : cudaLaunchKernelEx(&cfg, merge_kernel<1, 8>, mp);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail_cuda(e, "merge_kernel launch");
   if (g_prof_ev[2]) cudaEventRecord(g_prof_ev[2], st);
