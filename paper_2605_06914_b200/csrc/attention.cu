@@ -1527,6 +1527,10 @@ __device__ __forceinline__ void merge_slot(const MergeParams &p, int s, int r, i
 #define TAPER_MERGE_MIN_RPW 1  // 2: two slots per merge CTA at h = 1 (A/B: C2, C3 slower, C5 faster)
 #endif
 constexpr int kMergeMinRpw = TAPER_MERGE_MIN_RPW;
+#ifndef TAPER_MERGE_ONE_WAITER
+#define TAPER_MERGE_ONE_WAITER 0  // 1 (A/B): C5 h = 1 216.7 -> 212.3 us, C2 h = 1 37.0 -> 37.9: off
+#endif
+constexpr bool kMergeOneWaiter = TAPER_MERGE_ONE_WAITER;
 template <int RPW, int NB>
 __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1572,7 +1576,11 @@ __global__ void __launch_bounds__(kMergeThreads, 2) merge_kernel(MergeParams p) 
       *p.gcount = 0;  // re-armed before this kernel completes (the next merge waits for it)
     }
   }
-  pdl_wait();  // complete only after attend_kernel (its counter re-arm) has completed
+  // The merge grid must complete only after attend_kernel (its counter re-arm) has.  One
+  // CTA waiting would be enough and would let the others leave early, freeing SMs for the
+  // next call's attend CTAs -- which then also take SMs the merge CTAs not yet running
+  // need (TAPER_MERGE_ONE_WAITER, mixed: off)
+  if (!kMergeOneWaiter || blockIdx.x == gridDim.x - 1) pdl_wait();
   if (tr) {
     __syncwarp();
     unsigned long long g;
