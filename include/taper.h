@@ -269,9 +269,9 @@ TAPER_API int taper_build_work(const taper_batch *batch, const taper_admission *
  * An admitted slot with an empty context writes zero rows (TAPER_STATUS_EMPTY_CONTEXT).
  * Ordering contract (programmatic dependent launch): the kernels may start while the
  * previous kernel on `stream` is still running.  A work item may be resolved from the
- * work list before the grid dependency, but is used only after every work-list word it
- * was resolved from has been read again after the dependency and found unchanged
- * (otherwise it is resolved again); q / the K/V pools are read only after the grid
+ * work list before the grid dependency; its results are kept only if every work-list word
+ * it was resolved from reads the same after the dependency (otherwise they are discarded
+ * and the item is resolved again); q / the K/V pools are read only after the grid
  * dependency.  The page tables
  * (req_page_off ... seg_page_off) and the lengths in `batch` may be read early: they
  * must be written before the taper_admit / taper_build_work call that produced the work

@@ -853,7 +853,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t *it_full = ml_full + 2;             // [kItemRing] scheduler published an item
   uint64_t *it_empty = it_full + kItemRing;    // [kItemRing] all consumer warps are done
   uint64_t *sched_go = it_empty + kItemRing;   // K producer started an item -> scheduler
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sched_go + 1);
+  uint64_t *val_bar = sched_go + 1;            // scheduler validated record 0 -> epilogue
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sched_go + 2);
+  volatile int32_t *first_ok = reinterpret_cast<volatile int32_t *>(tmem_slot + 1);  // record 0 valid
   ItemRec *recs = reinterpret_cast<ItemRec *>(smem + kOffRec);
   float2 *xml = reinterpret_cast<float2 *>(smem + kOffML);
   const float *lpart = reinterpret_cast<const float *>(smem + kOffLPart);
@@ -896,6 +898,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_init(it_empty + i, kRingConsumers);
     }
     mbar_init(sched_go, 1);
+    mbar_init(val_bar, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -995,48 +998,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       return __shfl_sync(0xffffffffu, c, 0);
     };
     auto first_desc = [&]() -> int32_t { return lane < 8 ? snap : 0; };
-    for (uint32_t k = 0;; ++k) {
-      if (k >= 1) mbar_wait(sched_go, (k - 1) & 1);  // K producer started item k-1
-      int it = claim(k);
-      int32_t d = k == 0 ? first_desc() : load_desc(it);
-      if (k == 0 && lane == 0) trace_cta_dep(p, 13, d);  // descriptor loaded
-      const uint32_t slot = k % kItemRing;
-      ItemRec *rec = recs + slot;
-      mbar_wait(it_empty + slot, ((k / kItemRing) & 1) ^ 1);
-      int w, adm_off, g, slot_j;
-      for (bool early = k == 0;;) {
-        resolve(rec, it < n_items ? it : -1, d, w, adm_off, g, slot_j);
-        if (k == 0 && lane == 0) trace_cta(p, early ? 6 : 7);  // first record resolved
-        if (!early) break;
-        // The first record was resolved while the previous kernel drained.  Now wait for
-        // it (q, the K/V pools and a just-written work list become visible), let the merge
-        // kernel launch, and validate: the header, the descriptor, the branches' slots and
-        // (local item) the tile entries are loaded again -- independent loads, one latency
-        // -- and compared with the values the record was resolved from.
-        early = false;
-        pdl_wait();
-        pdl_launch_dependents();
-        if (lane == 0) trace_cta(p, 8);  // grid dependency resolved
-        const int32_t snap2 = __ldcg(snap_addr);
-        const bool was_item = it >= 0 && it < n_items;
-        const int nt_e = __shfl_sync(0xffffffffu, d, 6), tb_e = __shfl_sync(0xffffffffu, d, 4);
-        const bool local_e = __shfl_sync(0xffffffffu, d, 7) & kItemLocal;
-        const int sj2 = (was_item && lane < w) ? __ldcg(p.adm_by_req + adm_off + lane) : slot_j;
-        const int4 lt2 = (was_item && local_e && lane < nt_e) ? __ldcg(p.ltiles + tb_e + lane) : lt_seen;
-        const bool same = !TAPER_DBG_FORCE_RERESOLVE & (snap2 == snap) & (sj2 == slot_j) & (lt2.x == lt_seen.x) &
-                          (lt2.y == lt_seen.y) & (lt2.z == lt_seen.z) & (lt2.w == lt_seen.w);
-        if (__all_sync(0xffffffffu, same)) break;
-        snap = snap2;
-        derive();
-        it = claim(0);
-        d = first_desc();
-      }
-      if (it >= n_items) it = -1;
+    // publish record k (every lane arrives) and load its Q^T: box {64 d, 8 rows, 2 d-halves}
+    // of q viewed as (d-lo, GQA row, d-half, slot * h + g) -> [d-half][8 rows][128 B] per branch
+    auto publish = [&](uint32_t k, uint32_t slot, int it, int w, int g, int slot_j) {
       __syncwarp();
       mbar_arrive(it_full + slot);  // release (every lane): the record is visible
-      if (it < 0) break;
-      // Q^T of the item's w branches: box {64 d, 8 rows, 2 d-halves} of q viewed as
-      // (d-lo, GQA row, d-half, slot * h + g) -> [d-half][8 rows][128 B] per branch
+      if (it < 0) return;
       const uint32_t qb = k & 1;
       mbar_wait(q_free + qb, ((k >> 1) & 1) ^ 1);
       if (elect_one()) mbar_arrive_expect_tx(q_full + qb, w * 2048);
@@ -1046,6 +1013,63 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     slot_j * h + g);
       if (k == 0 && lane == 0) trace_cta(p, 9);  // first Q load issued
       __syncwarp();
+    };
+    bool redo = false;  // record 0 failed validation: record 1 is the first claim again
+    for (uint32_t k = 0;; ++k) {
+      if (k >= 1) mbar_wait(sched_go, (k - 1) & 1);  // K producer started item k-1
+      const bool first = k == 0 || (k == 1 && redo);
+      int it = claim(first ? 0 : k);
+      int32_t d = first ? first_desc() : load_desc(it);
+      if (k == 0 && lane == 0) trace_cta_dep(p, 13, d);  // descriptor loaded
+      const uint32_t slot = k % kItemRing;
+      ItemRec *rec = recs + slot;
+      mbar_wait(it_empty + slot, ((k / kItemRing) & 1) ^ 1);
+      int w, adm_off, g, slot_j;
+      resolve(rec, it < n_items ? it : -1, d, w, adm_off, g, slot_j);
+      if (k == 0 && lane == 0) trace_cta(p, 6);  // first record resolved
+      if (k == 0) {
+        // The first record was resolved while the previous kernel drained.  Wait for it (q,
+        // the K/V pools and a just-written work list become visible) and let the merge
+        // kernel launch.  A record that names an item is published at once; then the
+        // header, the descriptor, the branches' slots and (local item) the tile entries
+        // are loaded again -- independent loads, one latency -- and compared with the
+        // values it was resolved from.  On a difference the item runs anyway (its loads
+        // stay in bounds: TMA drops out-of-range boxes) but the epilogue discards its
+        // partials (first_ok = 0), and record 1 is the first claim resolved again.
+        pdl_wait();
+        pdl_launch_dependents();
+        if (lane == 0) trace_cta(p, 8);  // grid dependency resolved
+        const bool early_item = it >= 0 && it < n_items;
+        if (early_item) publish(0, slot, it, w, g, slot_j);
+        const int32_t snap2 = __ldcg(snap_addr);
+        const int nt_e = __shfl_sync(0xffffffffu, d, 6), tb_e = __shfl_sync(0xffffffffu, d, 4);
+        const bool local_e = __shfl_sync(0xffffffffu, d, 7) & kItemLocal;
+        const int sj2 = (early_item && lane < w) ? __ldcg(p.adm_by_req + adm_off + lane) : slot_j;
+        const int4 lt2 = (early_item && local_e && lane < nt_e) ? __ldcg(p.ltiles + tb_e + lane) : lt_seen;
+        const bool same = !TAPER_DBG_FORCE_RERESOLVE & (snap2 == snap) & (sj2 == slot_j) & (lt2.x == lt_seen.x) &
+                          (lt2.y == lt_seen.y) & (lt2.z == lt_seen.z) & (lt2.w == lt_seen.w);
+        const bool ok = __all_sync(0xffffffffu, same);
+        if (!ok) {
+          snap = snap2;
+          derive();
+        }
+        if (lane == 0) {
+          *first_ok = (!early_item || ok) ? 1 : 0;
+          mbar_arrive(val_bar);
+        }
+        if (early_item) {
+          redo = !ok;
+          continue;
+        }
+        if (!ok) {  // nothing published yet: resolve the first claim from the visible words
+          it = claim(0);
+          d = first_desc();
+          resolve(rec, it < n_items ? it : -1, d, w, adm_off, g, slot_j);
+        }
+      }
+      if (it >= n_items) it = -1;
+      publish(k, slot, it, w, g, slot_j);
+      if (it < 0) break;
     }
   } else if (warp == 0 || warp == 10) {
     // ======================= TMA producers: warp 0 = K, warp 10 = V =======================
@@ -1309,6 +1333,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t tO = tmem + lane_off + kColO + ob * 128;
       mbar_wait(ml_full + ob, (item_idx >> 1) & 1);
       mbar_wait(o_full + ob, (item_idx >> 1) & 1);
+      // record 0 was published before its validation: a record that failed it writes and
+      // publishes nothing (its item is resolved again as record 1)
+      bool keep = true;
+      if (item_idx == 0) {
+        mbar_wait(val_bar, 0);
+        keep = *first_ok != 0;
+        if (!keep) x.w = 0;
+      }
       if (warp == 6 && lane == 0) trace_ev(p, 10, 2048 + item_idx);
       if (tracing(p) && blockIdx.x == 0 && warp == 6 && lane == 0 &&
           2048 + int(item_idx) < p.trace_cap) {
@@ -1371,7 +1403,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (warp == 6 && lane == 0) trace_ev(p, 11, 2048 + item_idx);
       tc_fence_before();
       mbar_arrive(o_free + ob);
-      if (etid == 0) {
+      if (etid == 0 && keep) {
         __threadfence();
         atomicAdd(p.done + x.r * kGroup + x.g, 1);
       }
