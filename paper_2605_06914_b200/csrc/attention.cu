@@ -69,6 +69,10 @@ static_assert(kItemTiles <= 64, "scheduler lanes resolve at most two tiles each"
 #ifndef TAPER_MERGE_GRID
 #define TAPER_MERGE_GRID 0  // > 0: at most this many merge CTAs (A/B experiments)
 #endif
+#ifndef TAPER_CLAIM_LEAD
+#define TAPER_CLAIM_LEAD 8  // tiles before an item's end at which the next item is claimed
+#endif
+constexpr int kClaimLead = TAPER_CLAIM_LEAD;
 #ifndef TAPER_PDL
 #define TAPER_PDL 1  // 0: attend_kernel launches without PDL (A/B experiments)
 #endif
@@ -1092,15 +1096,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         break;
       }
       const ItemRec *rec = recs + (k % kItemRing);
-      if (is_k) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(sched_go);  // the scheduler may claim the next item
-      }
       const int g_u = rec->g;
       const int nt_u = rec->desc[6];
+      // the scheduler may claim the next item once this one's producer is kClaimLead tiles
+      // from its end (enough for the next record's dependent loads; an earlier claim keeps
+      // work reserved on a busy CTA while others run dry at the end of the queue)
+      const int t_go = nt_u > kClaimLead ? nt_u - kClaimLead : 0;
       // (Tiles issued in pairs by lanes 0 and 1 -- a higher TMA issue ceiling in isolation,
       // scripts/tma_issue_probe.cu -- measured 2.3 % slower on C2, r2 run l; one lane issues.)
       for (int t = 0; t < nt_u; ++t, ++n_prod) {
+        if (is_k && t == t_go) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(sched_go);
+        }
         const int tok0 = rec->tok0[t];
         const int valid = rec->valid[t];
         const uint32_t st = n_prod % n_stages;
