@@ -1,10 +1,11 @@
-"""The attention kernel resolves each CTA's first work item before its grid dependency and
-validates it afterwards by reloading the work-list words it was built from
-(include/taper.h ordering contract).  In practice the words match (the admission finished
-long before), so the re-resolve path is rarely taken; a test build forces it in every CTA
-(-DTAPER_DBG_FORCE_RERESOLVE=1).  Its outputs must equal the product build's bit for bit:
-the same record is resolved again from the same words, whatever the item type (row mode,
-swap mode, local items) or the rank's head count."""
+"""The attention kernel resolves each CTA's first work item before its grid dependency,
+publishes it as soon as the dependency resolves and validates it beside the first loads by
+reloading the work-list words it was built from (include/taper.h ordering contract).  In
+practice the words match (the admission finished long before), so the failure path -- the
+item runs, its epilogue discards it, and the first claim is resolved again as the next
+record -- is rarely taken; a test build forces it in every CTA
+(-DTAPER_DBG_FORCE_RERESOLVE=1).  Its outputs must equal the product build's bit for bit,
+whatever the item type (row mode, swap mode, local items) or the rank's head count."""
 import os
 import subprocess
 import sys
